@@ -1,0 +1,24 @@
+"""B200-native Discrete Projection Moment (DPM) hot path.
+
+A drop-in for the hot path of the reference package ``volmoments``
+(arXiv 2012.08099): the same public names for volumes, projections and 3D
+moments, with every stage running in hand-written sm_100a CUDA kernels behind
+the C ABI in include/dpm_b200.h.  There is no CPU fallback: without the CUDA
+library (paper_2012_08099_b200/libdpm_b200.so) and a GPU, compute calls raise.
+"""
+from .counters import OpCounters
+from .errors import FormatError, InconsistencyError
+from .moments3d import (ENGINES, MomentTensor3, count_ops, dpm_moments, dpm_moments_batch,
+                        moment_indices)
+from .projection import (ANGLES, Orientation, ProjectionImage, ProjectionSet, project, project_all,
+                         project_extended, project_subset, write_pgm)
+from .volume import Volume, delta, ellipsoid, random, uniform
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "ANGLES", "ENGINES", "FormatError", "InconsistencyError", "MomentTensor3", "OpCounters",
+    "Orientation", "ProjectionImage", "ProjectionSet", "Volume", "count_ops", "delta",
+    "dpm_moments", "dpm_moments_batch", "ellipsoid", "moment_indices", "project", "project_all",
+    "project_extended", "project_subset", "random", "uniform", "write_pgm",
+]

@@ -1,0 +1,76 @@
+// dpm_common.cuh -- shared geometry and launch plumbing for the DPM kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/dpm_b200.h"
+
+namespace dpm {
+
+// Stored image geometry and logical-origin offsets.  Index maps follow the
+// reference (projection.py:7-14): XY (x,y), YZ (y,z), ZX (z,x), DIAG (x+z,y),
+// ANTI (x-z+N-1,y); the order-5/6 extension adds X2P (x+2z,y) and
+// X2M (x-2z+2(N-1),y).  (ai, aj) shift stored indices to logical global
+// coordinates of a z-slab starting at global plane z0; for a whole
+// volume (z0 = 0) ai of ANTI is -(N-1), the reference's origin_offset
+// (projection.py:189-191, drt2d.py:196-208).
+struct ImageGeom { int64_t W, H, ai, aj; };
+
+__host__ __device__ inline ImageGeom image_geom(int64_t L, int64_t M, int64_t N, int64_t z0, int img) {
+  switch (img) {
+    case DPM_IMG_XY:   return {L, M, 0, 0};
+    case DPM_IMG_YZ:   return {M, N, 0, z0};
+    case DPM_IMG_ZX:   return {N, L, z0, 0};
+    case DPM_IMG_DIAG: return {L + N - 1, M, z0, 0};
+    case DPM_IMG_ANTI: return {L + N - 1, M, -(N - 1) - z0, 0};
+    case DPM_IMG_X2P:  return {L + 2 * N - 2, M, 2 * z0, 0};
+    default:           return {L + 2 * N - 2, M, -2 * (N - 1) - 2 * z0, 0};
+  }
+}
+
+__host__ __device__ inline int num_images(int order) { return order <= 3 ? 4 : order + 1; }
+__host__ __device__ inline int n2d(int order) { return (order + 1) * (order + 2) / 2; }
+__host__ __device__ inline int n3d(int order) { return (order + 1) * (order + 2) * (order + 3) / 6; }
+
+// p-major 2D moment slot: p then q (q <= K-p).
+__host__ __device__ inline int idx2(int order, int p, int q) { return p * (order + 1) - p * (p - 1) / 2 + q; }
+
+// lexicographic (p,q,r) slot == moment_indices (moments3d.py:46-54).
+__host__ __device__ inline int idx3(int order, int p, int q, int r) {
+  int n = 0;
+  for (int a = 0; a < p; ++a) { int s = order - a; n += (s + 1) * (s + 2) / 2; }
+  int s = order - p;
+  for (int b = 0; b < q; ++b) n += s - b + 1;
+  return n + r;
+}
+
+// Per-image pointer/geometry pack passed by value to kernels.
+struct ImageSet {
+  uint32_t* img[DPM_MAX_IMAGES];
+  int64_t W[DPM_MAX_IMAGES];
+  int64_t H[DPM_MAX_IMAGES];
+  int64_t ai[DPM_MAX_IMAGES];
+  int64_t aj[DPM_MAX_IMAGES];
+  int n_img;
+};
+
+template <typename T> struct VoxelTraits;
+template <> struct VoxelTraits<uint8_t>  { static __device__ __forceinline__ uint32_t get(uint8_t v, int32_t) { return v; } };
+template <> struct VoxelTraits<uint16_t> { static __device__ __forceinline__ uint32_t get(uint16_t v, int32_t) { return v; } };
+template <> struct VoxelTraits<int16_t>  { static __device__ __forceinline__ uint32_t get(int16_t v, int32_t off) { return (uint32_t)((int32_t)v + off); } };
+
+// thread-local count of kernels the last C-ABI call enqueued
+void note_launches(int n);
+void reset_launches();
+
+}  // namespace dpm
+
+#define DPM_CUDA_CHECK_LAUNCH()                                  \
+  do {                                                           \
+    cudaError_t _e = cudaGetLastError();                         \
+    if (_e != cudaSuccess) return DPM_ECUDA;                     \
+  } while (0)
+
+namespace dpm {
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
+}  // namespace dpm

@@ -1,0 +1,186 @@
+// moments2d.cu -- exact 2D raw moments of every projection image.
+//
+// M_pq = sum_j (j+aj)^q * sum_i I[j][i] (i+ai)^p   for p + q <= K.
+//
+// Replaces the reference's 1D-integral route (drt2d.integrals/assemble_2d,
+// drt2d.py:92-174, plus shift_origin :196-208 and exact.weighted_power_sums,
+// exact.py:63-82).  That route caps at 2D order 4; this one reaches the order 6
+// the extension needs and stays exact:
+//   stage 1 (per column i, per chunk of <= 256 rows):
+//       C_q[i] = sum_j I[j][i] (j+aj)^q, with (j+aj)^q split into 24-bit limbs
+//       held in a per-CTA shared table, so every product is one IMAD.WIDE.U32
+//       (32 x 24 -> 56 bits) accumulated into a uint64 that cannot overflow in
+//       256 rows;
+//   stage 2 (per column): C_q as a 128-bit integer times (i+ai)^p (signed),
+//       reduced over the CTA's columns and added into four 32-bit limb
+//       accumulators per moment with 64-bit atomics (exact, order independent).
+// The host checks the exactness envelope first (dpm_check_envelope), so every
+// partial sum is below 2^126 and arithmetic mod 2^128 is exact.
+#include <mutex>
+#include "dpm_common.cuh"
+
+namespace dpm {
+
+constexpr int M2_THREADS = 128;
+
+template <int JB> struct Limbs {
+  __host__ __device__ static constexpr int nl(int q) { return q == 0 ? 1 : (q * JB + 23) / 24; }
+  __host__ __device__ static constexpr int off(int q) { int s = 0; for (int a = 0; a < q; ++a) s += nl(a); return s; }
+};
+
+struct M2Params {
+  ImageSet s;
+  int64_t B;
+  int64_t rc;                              // rows per chunk (<= 256)
+  int64_t blocks_img[DPM_MAX_IMAGES + 1];  // prefix sums of blocks per image (per volume)
+  int64_t cblocks[DPM_MAX_IMAGES];         // column blocks per image
+  uint64_t* acc;                           // [B][n_img][n2][4]
+};
+
+template <int K, int JB>
+__global__ void __launch_bounds__(M2_THREADS) moments2d_kernel(M2Params p) {
+  using LP = Limbs<JB>;
+  constexpr int NT = LP::off(K + 1);        // total limbs across q = 0..K
+  constexpr int NTP = (NT + 3) & ~3;        // padded to uint4
+  constexpr int N2 = (K + 1) * (K + 2) / 2;
+  // table (stage 1) and red (stage 2) are live in disjoint phases: one buffer
+  extern __shared__ __align__(16) uint32_t m2_smem[];
+  uint32_t (*table)[NTP] = reinterpret_cast<uint32_t (*)[NTP]>(m2_smem);
+  uint32_t (*red)[M2_THREADS + 1] = reinterpret_cast<uint32_t (*)[M2_THREADS + 1]>(m2_smem);
+
+  const int64_t per_vol = p.blocks_img[p.s.n_img];
+  const int64_t b = blockIdx.x / per_vol;
+  int64_t r = blockIdx.x - b * per_vol;
+  int k = 0;
+  while (r >= p.blocks_img[k + 1]) ++k;
+  r -= p.blocks_img[k];
+  const int64_t rb = r / p.cblocks[k], cb = r - rb * p.cblocks[k];
+  const int64_t W = p.s.W[k], H = p.s.H[k], ai = p.s.ai[k], aj = p.s.aj[k];
+  const int64_t j0 = rb * p.rc;
+  const int rows = (int)imin64(p.rc, H - j0);
+  const int tid = threadIdx.x;
+
+  // row-power limb table: (j + aj)^q as 24-bit limbs
+  for (int rr = tid; rr < rows; rr += M2_THREADS) {
+    const unsigned __int128 y = (unsigned __int128)(uint64_t)(j0 + rr + aj);
+    unsigned __int128 pw = 1;
+    #pragma unroll
+    for (int q = 0; q <= K; ++q) {
+      unsigned __int128 t = pw;
+      #pragma unroll
+      for (int l = 0; l < LP::nl(q); ++l) { table[rr][LP::off(q) + l] = (uint32_t)(t & 0xFFFFFFu); t >>= 24; }
+      pw *= y;
+    }
+    #pragma unroll
+    for (int l = NT; l < NTP; ++l) table[rr][l] = 0;
+  }
+  __syncthreads();
+
+  const int64_t i = cb * M2_THREADS + tid;
+  uint64_t acc[NTP];
+  #pragma unroll
+  for (int l = 0; l < NTP; ++l) acc[l] = 0;
+  if (i < W) {
+    const uint32_t* col = p.s.img[k] + b * W * H + j0 * W + i;
+    #pragma unroll 4
+    for (int rr = 0; rr < rows; ++rr) {
+      const uint64_t v = __ldg(col + (int64_t)rr * W);
+      const uint4* tr = reinterpret_cast<const uint4*>(&table[rr][0]);
+      #pragma unroll
+      for (int l4 = 0; l4 < NTP / 4; ++l4) {
+        const uint4 t = tr[l4];
+        acc[4 * l4 + 0] += v * t.x;
+        acc[4 * l4 + 1] += v * t.y;
+        acc[4 * l4 + 2] += v * t.z;
+        acc[4 * l4 + 3] += v * t.w;
+      }
+    }
+  }
+
+  __syncthreads();  // table dead from here on; its storage becomes red
+  // stage 2: C_q (mod 2^128) times (i + ai)^p, p + q <= K
+  unsigned __int128 C[K + 1];
+  #pragma unroll
+  for (int q = 0; q <= K; ++q) {
+    unsigned __int128 c = 0;
+    #pragma unroll
+    for (int l = 0; l < LP::nl(q); ++l) c += ((unsigned __int128)acc[LP::off(q) + l]) << (24 * l);
+    C[q] = c;
+  }
+  const __int128 x = (__int128)(i + ai);
+  __int128 xp = 1;
+  int m = 0;
+  #pragma unroll
+  for (int pp = 0; pp <= K; ++pp) {
+    #pragma unroll
+    for (int q = 0; q <= K - pp; ++q) {
+      unsigned __int128 v = (i < W) ? C[q] * (unsigned __int128)xp : 0;
+      red[4 * m + 0][tid] = (uint32_t)v;
+      red[4 * m + 1][tid] = (uint32_t)(v >> 32);
+      red[4 * m + 2][tid] = (uint32_t)(v >> 64);
+      red[4 * m + 3][tid] = (uint32_t)(v >> 96);
+      ++m;
+    }
+    xp *= x;
+  }
+  __syncthreads();
+  uint64_t* out = p.acc + ((b * p.s.n_img + k) * N2) * 4;
+  for (int e = tid; e < N2 * 4; e += M2_THREADS) {
+    uint64_t s = 0;
+    #pragma unroll 8
+    for (int t = 0; t < M2_THREADS; ++t) s += red[e][t];
+    if (s) atomicAdd(reinterpret_cast<unsigned long long*>(out + e), (unsigned long long)s);
+  }
+}
+
+template <int K, int JB>
+static void launch_kj(dim3 grid, cudaStream_t st, const M2Params& p) {
+  constexpr int NT = Limbs<JB>::off(K + 1);
+  constexpr int NTP = (NT + 3) & ~3;
+  constexpr int N2 = (K + 1) * (K + 2) / 2;
+  constexpr size_t t_bytes = 256 * NTP * 4, r_bytes = (size_t)N2 * 4 * (M2_THREADS + 1) * 4;
+  constexpr size_t bytes = t_bytes > r_bytes ? t_bytes : r_bytes;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(moments2d_kernel<K, JB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  });
+  moments2d_kernel<K, JB><<<grid, M2_THREADS, bytes, st>>>(p);
+}
+
+template <int K>
+static void launch_k(int jb, dim3 grid, cudaStream_t st, const M2Params& p) {
+  if (jb <= 12) launch_kj<K, 12>(grid, st, p);
+  else if (jb <= 16) launch_kj<K, 16>(grid, st, p);
+  else launch_kj<K, 21>(grid, st, p);
+}
+
+int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_t* acc, cudaStream_t st) {
+  M2Params p;
+  p.s = s; p.B = B; p.acc = acc;
+  // rows per chunk: fewer rows -> more CTAs for short images
+  int64_t px = 0, maxH = 0;
+  for (int k = 0; k < s.n_img; ++k) { px += s.W[k] * s.H[k]; maxH = s.H[k] > maxH ? s.H[k] : maxH; }
+  p.rc = (px * B < (int64_t)(1 << 22)) ? 64 : 256;
+  p.blocks_img[0] = 0;
+  for (int k = 0; k < s.n_img; ++k) {
+    p.cblocks[k] = (s.W[k] + M2_THREADS - 1) / M2_THREADS;
+    const int64_t rblocks = (s.H[k] + p.rc - 1) / p.rc;
+    p.blocks_img[k + 1] = p.blocks_img[k] + p.cblocks[k] * rblocks;
+  }
+  for (int k = s.n_img + 1; k <= DPM_MAX_IMAGES; ++k) p.blocks_img[k] = p.blocks_img[s.n_img];
+  const int64_t nblocks = p.blocks_img[s.n_img] * B;
+  if (nblocks == 0) return DPM_OK;
+  if (nblocks > 0x7fffffffLL) return DPM_EINVAL;
+  dim3 grid((unsigned)nblocks);
+  switch (order) {
+    case 3: launch_k<3>(jbits, grid, st, p); break;
+    case 4: launch_k<4>(jbits, grid, st, p); break;
+    case 5: launch_k<5>(jbits, grid, st, p); break;
+    default: launch_k<6>(jbits, grid, st, p); break;
+  }
+  note_launches(1);
+  DPM_CUDA_CHECK_LAUNCH();
+  return DPM_OK;
+}
+
+}  // namespace dpm

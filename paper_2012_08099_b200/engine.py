@@ -1,0 +1,213 @@
+"""Device pipeline: torch provides device memory and streams; every stage runs
+in the CUDA kernels behind the C ABI (paper_2012_08099_b200/_native.py).
+
+Voxel tensors are CUDA tensors of dtype uint8 / uint16 / int16 (int16 with an
+``offset``, e.g. +1024 for CT data), shaped [N, M, L] or [B, N, M, L] and
+contiguous along x.  Exact 128-bit results come back as int64 (lo, hi) pairs.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+
+_TORCH_DTYPE = {torch.uint8: nat.DPM_U8, torch.uint16: nat.DPM_U16, torch.int16: nat.DPM_I16}
+_VMAX = {nat.DPM_U8: 255, nat.DPM_U16: 65535, nat.DPM_I16: 65535}
+
+
+def check_order(order: int) -> None:
+    """Orders 3..6 (the reference accepts 3 and 4, moments3d.py:57-59; 5 and 6
+    are this build's extension)."""
+    if not isinstance(order, (int, np.integer)) or not 3 <= int(order) <= nat.MAX_ORDER:
+        raise ValueError(f"order must be in 3..{nat.MAX_ORDER}, got {order}")
+
+
+def num_images(order: int) -> int:
+    return 4 if order <= 3 else order + 1
+
+
+def n2d(order: int) -> int:
+    return (order + 1) * (order + 2) // 2
+
+
+def n3d(order: int) -> int:
+    return (order + 1) * (order + 2) * (order + 3) // 6
+
+
+def stream_handle(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def make_desc(vox: torch.Tensor, offset: int = 0, z0: int = 0) -> nat.VolumeDesc:
+    """C-ABI descriptor of a [N,M,L] or [B,N,M,L] voxel tensor (x-contiguous)."""
+    if vox.dtype not in _TORCH_DTYPE:
+        raise ValueError(f"unsupported voxel dtype {vox.dtype}; use uint8, uint16 or int16(+offset)")
+    if vox.dim() == 3:
+        n, m, l = vox.shape
+        b, sb = 1, vox.numel()
+        sz, sy, sx = vox.stride()
+    elif vox.dim() == 4:
+        b, n, m, l = vox.shape
+        sb, sz, sy, sx = vox.stride()
+    else:
+        raise ValueError(f"voxel tensor must be 3D or 4D, got {vox.dim()}D")
+    if sx != 1:
+        raise ValueError("voxel rows must be contiguous along x")
+    d = nat.VolumeDesc()
+    d.L, d.M, d.N, d.B = int(l), int(m), int(n), int(b)
+    d.stride_y, d.stride_z, d.stride_b = int(sy), int(sz), int(sb)
+    d.dtype = _TORCH_DTYPE[vox.dtype]
+    d.offset = int(offset)
+    d.z0 = int(z0)
+    return d
+
+
+def check_envelope(L: int, M: int, N_global: int, dtype_code: int, order: int) -> None:
+    nat.check(nat.lib().dpm_check_envelope(L, M, N_global, _VMAX[dtype_code], order),
+              f"dims ({L}, {M}, {N_global}) at order {order}")
+
+
+class _Workspace:
+    """Per-device scratch buffer reused across calls (grow-only)."""
+
+    def __init__(self):
+        self._bufs: dict[tuple[int, int], torch.Tensor] = {}
+        self._lock = threading.Lock()
+
+    def get(self, nbytes: int, device: torch.device) -> torch.Tensor:
+        key = (device.index if device.index is not None else torch.cuda.current_device(), threading.get_ident())
+        with self._lock:
+            buf = self._bufs.get(key)
+            if buf is None or buf.numel() < nbytes:
+                buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+                self._bufs[key] = buf
+            return buf
+
+
+_WS = _Workspace()
+
+
+@dataclass
+class DeviceMoments:
+    """Result of the device pipeline for B volumes."""
+    i128: torch.Tensor     # [B, n3d, 2] int64 (lo, hi) exact
+    f64: torch.Tensor      # [B, n3d] float64, correctly rounded from i128 (to ~1 ulp)
+    status: torch.Tensor   # [B] int32 DPM_ST_* bits
+    launches: int
+
+
+def image_layout(desc: nat.VolumeDesc, img: int) -> tuple[int, int, int, int]:
+    out = [ctypes.c_int64() for _ in range(4)]
+    nat.check(nat.lib().dpm_image_layout(ctypes.byref(desc), img, *[ctypes.byref(o) for o in out]),
+              "dpm_image_layout")
+    return tuple(int(o.value) for o in out)
+
+
+def project(vox: torch.Tensor, n_img: int, offset: int = 0, z0: int = 0,
+            stream: torch.cuda.Stream | None = None) -> list[torch.Tensor]:
+    """Projection images 0..n_img-1 as int32 tensors [B, H, W] holding uint32 bits."""
+    desc = make_desc(vox, offset, z0)
+    imgs = []
+    for k in range(n_img):
+        W, H, _, _ = image_layout(desc, k)
+        imgs.append(torch.empty((desc.B, H, W), dtype=torch.int32, device=vox.device))
+    ptrs = (ctypes.c_void_p * n_img)(*[t.data_ptr() for t in imgs])
+    wsb = int(nat.lib().dpm_project_workspace_bytes(ctypes.byref(desc), n_img))
+    ws = _WS.get(wsb, vox.device) if wsb else None
+    nat.check(nat.lib().dpm_project(ctypes.byref(desc), vox.data_ptr(), n_img, ptrs,
+                                    ws.data_ptr() if ws is not None else None, wsb, stream_handle(stream)),
+              "dpm_project")
+    return imgs
+
+
+def moments(vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0, n_global: int | None = None,
+            stream: torch.cuda.Stream | None = None, out: DeviceMoments | None = None) -> DeviceMoments:
+    """Whole pipeline (project -> exact 2D moments -> device epilogue)."""
+    check_order(order)
+    desc = make_desc(vox, offset, z0)
+    check_envelope(desc.L, desc.M, n_global if n_global is not None else desc.N + desc.z0, desc.dtype, order)
+    lib = nat.lib()
+    wsb = int(lib.dpm_workspace_bytes(ctypes.byref(desc), order))
+    if wsb == 0:
+        raise ValueError("invalid volume descriptor")
+    ws = _WS.get(wsb, vox.device)
+    if out is None:
+        out = DeviceMoments(
+            i128=torch.empty((desc.B, n3d(order), 2), dtype=torch.int64, device=vox.device),
+            f64=torch.empty((desc.B, n3d(order)), dtype=torch.float64, device=vox.device),
+            status=torch.empty((desc.B,), dtype=torch.int32, device=vox.device),
+            launches=0)
+    nat.check(lib.dpm_moments(ctypes.byref(desc), vox.data_ptr(), order, ws.data_ptr(), wsb,
+                              out.i128.data_ptr(), out.f64.data_ptr(), out.status.data_ptr(),
+                              stream_handle(stream)), "dpm_moments")
+    out.launches = nat.last_launch_count()
+    return out
+
+
+def moments2d_partial(vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0,
+                      stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Project + exact 2D moments of a slab in GLOBAL coordinates; returns the
+    limb accumulator [B, n_img, n2d, 4] (int64 storage of uint64 sums).  Limb
+    accumulators of z-slabs add elementwise (moments are linear in voxels)."""
+    check_order(order)
+    n_img = num_images(order)
+    imgs = project(vox, n_img, offset, z0, stream)
+    desc = make_desc(vox, offset, z0)
+    acc = torch.empty((desc.B, n_img, n2d(order), 4), dtype=torch.int64, device=vox.device)
+    ptrs = (ctypes.c_void_p * n_img)(*[t.data_ptr() for t in imgs])
+    nat.check(nat.lib().dpm_moments2d(ctypes.byref(desc), n_img, ptrs, order, acc.data_ptr(),
+                                      stream_handle(stream)), "dpm_moments2d")
+    return acc
+
+
+def derive(acc: torch.Tensor, order: int, stream: torch.cuda.Stream | None = None) -> DeviceMoments:
+    """Device epilogue on a (possibly summed) limb accumulator."""
+    check_order(order)
+    B = acc.shape[0]
+    desc = nat.VolumeDesc()
+    desc.L = desc.M = desc.N = 1
+    desc.B = B
+    dev = acc.device
+    out = DeviceMoments(
+        i128=torch.empty((B, n3d(order), 2), dtype=torch.int64, device=dev),
+        f64=torch.empty((B, n3d(order)), dtype=torch.float64, device=dev),
+        status=torch.empty((B,), dtype=torch.int32, device=dev), launches=0)
+    nat.check(nat.lib().dpm_derive3d(ctypes.byref(desc), acc.data_ptr(), order, out.i128.data_ptr(),
+                                     out.f64.data_ptr(), out.status.data_ptr(), stream_handle(stream)),
+              "dpm_derive3d")
+    out.launches = nat.last_launch_count()
+    return out
+
+
+def i128_to_ints(pairs: np.ndarray) -> list[int]:
+    """[n, 2] int64 (lo, hi) -> exact Python ints."""
+    lo = pairs[..., 0].astype(np.uint64).ravel().tolist()
+    hi = pairs[..., 1].ravel().tolist()
+    return [h * (1 << 64) + l for l, h in zip(lo, hi)]
+
+
+def acc_to_ints(acc: np.ndarray) -> np.ndarray:
+    """Limb accumulator [..., 4] (uint64 sums of 32-bit limbs) -> object array of ints."""
+    a = acc.astype(np.uint64)
+    flat = a.reshape(-1, 4).tolist()
+    vals = []
+    for l0, l1, l2, l3 in flat:
+        v = (l0 + (l1 << 32) + (l2 << 64) + (l3 << 96)) % (1 << 128)
+        vals.append(v - (1 << 128) if v >= (1 << 127) else v)
+    return np.array(vals, dtype=object).reshape(acc.shape[:-1])
+
+
+def synth_noise(L: int, M: int, z0: int, n_planes: int, seed: int, device=None,
+                stream: torch.cuda.Stream | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Config-5 smooth-noise slab [n_planes, M, L] uint16 generated on the device."""
+    if out is None:
+        out = torch.empty((n_planes, M, L), dtype=torch.uint16, device=device or "cuda")
+    nat.check(nat.lib().dpm_synth_noise_u16(out.data_ptr(), L, M, z0, n_planes, seed & ((1 << 64) - 1),
+                                            stream_handle(stream)), "dpm_synth_noise_u16")
+    return out
