@@ -1,10 +1,549 @@
-// project_stream.cu -- streaming projection kernel (placeholder: generic path only).
+// project_stream.cu -- the streaming projection pass (one read of every voxel).
+//
+// Replaces projection._accumulate (projection.py:139-186), which sweeps the
+// volume at least four times (three numpy reductions plus a chunked shear
+// copy), with a single pass that builds all P images at once (the paper's
+// Listing 1).
+//
+// Decomposition ("K1 project_stream"):
+//   column   = (volume b, x-tile of 256 voxels, z-tile of 64 planes)
+//   row-step = one y of one column: a 256 (x) x 64 (z) slice of plane-rows,
+//              fetched by ONE 4-D TMA box (x 256, y 1, z 64, b 1) into a
+//              shared-memory stage; a STAGES-deep mbarrier pipeline keeps
+//              several row-steps in flight per SM (zero-filled out of bounds).
+//   CTA      = 8 warps; warp w owns planes Z0+8w..+7, lane l owns x = X0+8l..+7,
+//              so each lane reduces an 8 (x) x 8 (z) patch per row-step.
+//   ZX (x,z)  sum over y: 64 registers per lane, persistent across the
+//             row-steps of a column, flushed with red.global on column change.
+//   XY and the oblique images (x + t z, y), t = 1, -1, 2, -2: plane pairs are
+//             folded into 8 / 15 / 22-cell register windows with 3-input adds,
+//             window overlap with lane+1 (+2) goes over warp shuffles, and each
+//             lane adds its 8 owned cells into the CTA's shared-memory row with
+//             red.shared (8 warps = 8 z-blocks of the same row).  After the
+//             row-step barrier the row is flushed to global memory with one
+//             coalesced red.global per non-zero cell and re-zeroed
+//             (double-buffered rows, one __syncthreads per row-step).
+//   YZ (y,z)  per-plane lane sums, warp reduce-scatter, one red.global per (z,y).
+// Work split: row-steps are grouped into y-bands sized so a band's image rows
+// stay L2-resident; within a band the (column, y) sequence is cut into equal
+// contiguous runs, one per persistent CTA.
+// Exactness: uint32 ray sums (the C ABI rejects shapes whose longest ray could
+// reach 2^32) and associative integer atomics: bit-identical to the reference.
+#include <cudaTypedefs.h>
+#include <mutex>
 #include "dpm_common.cuh"
+#include "ptx.cuh"
+
 namespace dpm {
+
+constexpr int SX = 256;                // x-tile (elements)
+constexpr int SZ = 64;                 // z-tile (planes)
+constexpr int W1 = SX + SZ - 1;        // DIAG/ANTI row footprint of a tile (319)
+constexpr int W2 = SX + 2 * SZ - 2;    // X2P/X2M row footprint (382)
+constexpr int W1P = 320, W2P = 384;    // padded
+constexpr int THREADS = 512;   // 16 warps: 8 axis warps + 8 oblique warps
+
+struct StreamParams {
+  int64_t L, M, N, B;
+  int32_t offset;
+  int64_t ntx, ntz, ncol;      // tiles along x, z; columns = B * ntz * ntx
+  int64_t band;                // rows per y-band
+  ImageSet s;
+};
+
+template <typename T> struct Vec;
+template <> struct Vec<uint16_t> { using type = uint4; };
+template <> struct Vec<int16_t>  { using type = uint4; };
+template <> struct Vec<uint8_t>  { using type = uint2; };
+
+template <typename T> __device__ __forceinline__ void unpack8(const typename Vec<T>::type& d, uint32_t* v, int32_t off);
+template <> __device__ __forceinline__ void unpack8<uint16_t>(const uint4& d, uint32_t* v, int32_t) {
+  const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+  #pragma unroll
+  for (int i = 0; i < 4; ++i) { v[2 * i] = w[i] & 0xFFFFu; v[2 * i + 1] = w[i] >> 16; }
+}
+template <> __device__ __forceinline__ void unpack8<int16_t>(const uint4& d, uint32_t* v, int32_t off) {
+  const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+  #pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[2 * i] = (uint32_t)((int32_t)(int16_t)(w[i] & 0xFFFFu) + off);
+    v[2 * i + 1] = (uint32_t)((int32_t)(int16_t)(w[i] >> 16) + off);
+  }
+}
+template <> __device__ __forceinline__ void unpack8<uint8_t>(const uint2& d, uint32_t* v, int32_t) {
+  const uint32_t w[2] = {d.x, d.y};
+  #pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    #pragma unroll
+    for (int j = 0; j < 4; ++j) v[4 * i + j] = (w[i] >> (8 * j)) & 0xFFu;
+  }
+}
+
+// win[c] += a[c - OA] + b[c - OB] for every window cell the plane pair
+// (a = plane t, b = plane t+1) reaches.  Called with OA/OB that are constants
+// after unrolling, so every index is resolved at compile time (3-input adds).
+//   DIAG c = k + t:        OA = t,        OB = t + 1
+//   ANTI c = k - t + 7:    OA = 7 - t,    OB = 6 - t
+//   X2P  c = k + 2t:       OA = 2t,       OB = 2t + 2
+//   X2M  c = k - 2t + 14:  OA = 14 - 2t,  OB = 12 - 2t
+template <int NW>
+__device__ __forceinline__ void fold_pair(uint32_t* win, const uint32_t* a, const uint32_t* b, int OA, int OB) {
+  #pragma unroll
+  for (int c = 0; c < NW; ++c) {
+    const int ka = c - OA, kb = c - OB;
+    const bool ha = ka >= 0 && ka < 8, hb = kb >= 0 && kb < 8;
+    if (ha && hb) win[c] += a[ka] + b[kb];
+    else if (ha) win[c] += a[ka];
+    else if (hb) win[c] += b[kb];
+  }
+}
+
+// Window cells [8, 16) belong to lane+1 and [16, 24) to lane+2: shuffle them up
+// and add into the receiver's owned cells [0, 8).  The sender keeps its copy in
+// spill[] (lanes 31/30 add theirs to the CTA row: it belongs to the next tile).
+template <int NW>
+__device__ __forceinline__ void merge_spill(uint32_t* win, uint32_t* spill, int lane) {
+  #pragma unroll
+  for (int c = 8; c < NW; ++c) {
+    const int dl = c >> 3;
+    const uint32_t in = __shfl_up_sync(0xffffffffu, win[c], dl);
+    spill[c - 8] = win[c];
+    win[c & 7] += (lane >= dl) ? in : 0u;
+  }
+}
+
+template <int NW>
+__device__ __forceinline__ void merge_owned(uint32_t* win, int lane) {
+  #pragma unroll
+  for (int c = 8; c < NW; ++c) {
+    const int dl = c >> 3;
+    const uint32_t in = __shfl_up_sync(0xffffffffu, win[c], dl);
+    win[c & 7] += (lane >= dl) ? in : 0u;
+  }
+}
+
+template <int NW>
+__device__ __forceinline__ void add_owned(uint32_t addr, const uint32_t* win) {
+  ptx::red_shared_add<0>(addr, win[0]);  ptx::red_shared_add<4>(addr, win[1]);
+  ptx::red_shared_add<8>(addr, win[2]);  ptx::red_shared_add<12>(addr, win[3]);
+  ptx::red_shared_add<16>(addr, win[4]); ptx::red_shared_add<20>(addr, win[5]);
+  ptx::red_shared_add<24>(addr, win[6]); ptx::red_shared_add<28>(addr, win[7]);
+}
+
+template <int NS>
+__device__ __forceinline__ void add_spill(uint32_t addr, const uint32_t* spill, int first) {
+  #pragma unroll
+  for (int c = 0; c < NS; ++c)
+    if (c >= first) ptx::red_shared_add_dyn(addr + 32 + 4 * c, spill[c]);
+}
+
+// Per-CTA cursor over its row-steps: bands in order; inside a band the CTA's
+// contiguous run of the (column, y) sequence.  Advances incrementally (the
+// 64-bit divisions happen once per band, not per row-step).
+struct Cursor {
+  int32_t y0, yb, c, yoff, left;
+  bool done;
+  __device__ void band_setup(const StreamParams& p) {
+    while (y0 < p.M) {
+      yb = (int32_t)imin64(p.band, p.M - y0);
+      const int64_t seq = p.ncol * yb;
+      const int64_t s = (seq * blockIdx.x) / gridDim.x;
+      const int64_t e = (seq * (blockIdx.x + 1)) / gridDim.x;
+      if (s < e) { c = (int32_t)(s / yb); yoff = (int32_t)(s - (int64_t)c * yb); left = (int32_t)(e - s); done = false; return; }
+      y0 += (int32_t)p.band;
+    }
+    done = true;
+  }
+  __device__ void init(const StreamParams& p) { y0 = 0; band_setup(p); }
+  __device__ __forceinline__ void advance(const StreamParams& p) {
+    if (--left == 0) { y0 += (int32_t)p.band; band_setup(p); return; }
+    if (++yoff == yb) { yoff = 0; ++c; }
+  }
+  __device__ __forceinline__ int32_t y() const { return y0 + yoff; }
+};
+
+// CTA-row regions (words) for one parity: XY | DIAG | ANTI | X2P | X2M
+template <int NI> struct RowLayout {
+  static constexpr int XY = 0, DG = SX, AN = SX + W1P, XP = SX + 2 * W1P, XM = SX + 2 * W1P + W2P;
+  static constexpr int WORDS = NI <= 4 ? SX + W1P : NI == 5 ? SX + 2 * W1P : NI == 6 ? SX + 2 * W1P + W2P
+                                                                                   : SX + 2 * W1P + 2 * W2P;
+};
+
+template <typename T>
+__device__ __forceinline__ void load_pair(const T* tile, int t0, uint32_t* a, uint32_t* bb, int32_t off, bool xok, int zc) {
+  using V = typename Vec<T>::type;
+  unpack8<T>(*reinterpret_cast<const V*>(tile + t0 * SX), a, off);
+  unpack8<T>(*reinterpret_cast<const V*>(tile + (t0 + 1) * SX), bb, off);
+  if (((T)-1) < (T)0) {  // signed input: zero-filled (out-of-bounds) voxels must stay 0 after the offset
+    const bool ok0 = xok && t0 < zc, ok1 = xok && t0 + 1 < zc;
+    #pragma unroll
+    for (int k = 0; k < 8; ++k) { a[k] = ok0 ? a[k] : 0u; bb[k] = ok1 ? bb[k] : 0u; }
+  }
+}
+
+// Per-CTA pipeline state: TMA stages (full barriers), double-buffered CTA rows.
+// One __syncthreads per row-step separates "add into rows[parity]" from
+// "flush rows[parity]" and frees the consumed stage for the producer.
+template <typename T, int NI, int STAGES>
+struct Pipe {
+  using RL = RowLayout<NI>;
+  static constexpr uint32_t STAGE_BYTES = SZ * SX * sizeof(T);
+  const StreamParams* p;
+  const CUtensorMap* tmap;
+  uint8_t* stages;
+  uint32_t* rows;
+  uint64_t* full;
+  uint32_t rows_addr;
+  int tid;
+  Cursor prod;   // producer (thread 0)
+  int pst;
+
+  __device__ __forceinline__ void issue() {
+    const int32_t per = (int32_t)(p->ntz * p->ntx);
+    const int32_t b = prod.c / per, r = prod.c - b * per;
+    const int32_t zt = r / (int32_t)p->ntx;
+    ptx::mbar_arrive_expect_tx(&full[pst], STAGE_BYTES);
+    ptx::tma_load_4d(stages + pst * STAGE_BYTES, tmap, &full[pst], (r - zt * (int32_t)p->ntx) * SX, prod.y(), zt * SZ, b);
+    prod.advance(*p);
+    if (++pst == STAGES) pst = 0;
+  }
+
+  // after the row-step barrier: refill the consumed stage, flush the CTA rows (4 cells per thread-op)
+  __device__ __forceinline__ void end_step(int parity, int32_t col, int32_t y) {
+    if (tid == 0 && !prod.done) issue();
+    const int32_t per = (int32_t)(p->ntz * p->ntx);
+    const int32_t b = col / per, r = col - b * per;
+    const int64_t Z0 = (int64_t)(r / (int32_t)p->ntx) * SZ, X0 = (int64_t)(r % (int32_t)p->ntx) * SX;
+    uint32_t* rw = rows + parity * RL::WORDS;
+    const int64_t rowid = (int64_t)b * p->M + y;
+    #pragma unroll
+    for (int j = 0; j < (RL::WORDS / 4 + THREADS - 1) / THREADS; ++j) {
+      const int f = 4 * (tid + j * THREADS);
+      if (f < RL::WORDS) {
+        const uint4 v4 = *reinterpret_cast<uint4*>(rw + f);
+        *reinterpret_cast<uint4*>(rw + f) = make_uint4(0, 0, 0, 0);
+        int i, rlo = 0, rhi;
+        int64_t g0;
+        uint32_t* g;
+        if (f < RL::DG) {
+          i = f; g0 = X0; rhi = (int)imin64(SX, p->L - X0);
+          g = p->s.img[DPM_IMG_XY] + rowid * p->L;
+        } else if (f < RL::AN) {
+          const int64_t W = p->s.W[DPM_IMG_DIAG];
+          i = f - RL::DG; g0 = X0 + Z0; rhi = (int)imin64(W1, W - g0);
+          g = p->s.img[DPM_IMG_DIAG] + rowid * W;
+        } else if (NI <= DPM_IMG_X2P || f < RL::XP) {
+          const int64_t W = p->s.W[DPM_IMG_ANTI];
+          i = f - RL::AN; g0 = X0 - Z0 - 63 + p->N - 1; rlo = (int)imax64(0, -g0); rhi = (int)imin64(W1, W - g0);
+          g = p->s.img[DPM_IMG_ANTI] + rowid * W;
+        } else if (NI <= DPM_IMG_X2M || f < RL::XM) {
+          const int64_t W = p->s.W[DPM_IMG_X2P];
+          i = f - RL::XP; g0 = X0 + 2 * Z0; rhi = (int)imin64(W2, W - g0);
+          g = p->s.img[DPM_IMG_X2P] + rowid * W;
+        } else {
+          const int64_t W = p->s.W[DPM_IMG_X2M];
+          i = f - RL::XM; g0 = X0 - 2 * Z0 - 126 + 2 * (p->N - 1); rlo = (int)imax64(0, -g0); rhi = (int)imin64(W2, W - g0);
+          g = p->s.img[DPM_IMG_X2M] + rowid * W;
+        }
+        uint32_t* gp = g + g0 + i;
+        ptx::red_global_add_if(gp + 0, v4.x, v4.x != 0 && i + 0 >= rlo && i + 0 < rhi);
+        ptx::red_global_add_if(gp + 1, v4.y, v4.y != 0 && i + 1 >= rlo && i + 1 < rhi);
+        ptx::red_global_add_if(gp + 2, v4.z, v4.z != 0 && i + 2 >= rlo && i + 2 < rhi);
+        ptx::red_global_add_if(gp + 3, v4.w, v4.w != 0 && i + 3 >= rlo && i + 3 < rhi);
+      }
+    }
+  }
+};
+
+struct ColGeom {
+  int64_t X0, Z0;
+  int32_t b;
+  int zc;
+  bool xok;
+  __device__ __forceinline__ void set(const StreamParams& p, int32_t col, int w, int lane) {
+    const int32_t per = (int32_t)(p.ntz * p.ntx);
+    b = col / per;
+    const int32_t r = col - b * per;
+    Z0 = (int64_t)(r / (int32_t)p.ntx) * SZ;
+    X0 = (int64_t)(r % (int32_t)p.ntx) * SX;
+    zc = (int)imax64(0, imin64(8, p.N - (Z0 + 8 * w)));
+    xok = X0 + 8 * lane < p.L;
+  }
+};
+
+// Axis warps (0..7): ZX registers, XY column sums, YZ plane sums.
+template <typename T, int NI, int STAGES>
+__device__ __forceinline__ void axis_loop(Pipe<T, NI, STAGES>& pp, int w, int lane) {
+  using RL = RowLayout<NI>;
+  const StreamParams& p = *pp.p;
+  Cursor cur;
+  cur.init(p);
+  uint32_t zx[8][8];
+  int32_t col = -1;
+  ColGeom g;
+  g.zc = 0; g.xok = false;
+  uint32_t* zx_col = nullptr;
+  uint32_t* yz_col = nullptr;
+  int cst = 0, parity = 0;
+  uint32_t cphase = 0;
+  auto flush_zx = [&]() {
+    if (col < 0) return;
+    #pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      #pragma unroll
+      for (int t = 0; t < 8; ++t)
+        ptx::red_global_add_if(zx_col + k * p.N + t, zx[t][k], zx[t][k] != 0 && g.xok && t < g.zc);
+    }
+  };
+  while (!cur.done) {
+    const int32_t y = cur.y();
+    if (cur.c != col) {
+      flush_zx();
+      col = cur.c;
+      g.set(p, col, w, lane);
+      #pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        #pragma unroll
+        for (int k = 0; k < 8; ++k) zx[t][k] = 0;
+      }
+      zx_col = p.s.img[DPM_IMG_ZX] + (int64_t)g.b * p.L * p.N + (g.X0 + 8 * lane) * p.N + g.Z0 + 8 * w;
+      yz_col = p.s.img[DPM_IMG_YZ] + (int64_t)g.b * p.M * p.N + (g.Z0 + 8 * w + (lane >> 2)) * p.M;
+    }
+    ptx::mbar_wait(&pp.full[cst], cphase);
+    const T* tile = reinterpret_cast<const T*>(pp.stages + cst * Pipe<T, NI, STAGES>::STAGE_BYTES) + (8 * w) * SX + 8 * lane;
+    uint32_t cs[8], r8[8];
+    #pragma unroll
+    for (int i = 0; i < 8; ++i) cs[i] = 0;
+    #pragma unroll
+    for (int tp = 0; tp < 4; ++tp) {
+      const int t0 = 2 * tp, t1 = t0 + 1;
+      uint32_t a[8], bb[8];
+      load_pair<T>(tile, t0, a, bb, p.offset, g.xok, g.zc);
+      #pragma unroll
+      for (int k = 0; k < 8; ++k) { zx[t0][k] += a[k]; zx[t1][k] += bb[k]; cs[k] += a[k] + bb[k]; }
+      r8[t0] = (a[0] + a[1] + a[2]) + (a[3] + a[4] + a[5]) + (a[6] + a[7]);
+      r8[t1] = (bb[0] + bb[1] + bb[2]) + (bb[3] + bb[4] + bb[5]) + (bb[6] + bb[7]);
+    }
+    // YZ: warp reduce-scatter of the 8 plane sums; lane quad q ends with plane q's total
+    const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+    uint32_t r4[4], r2[2], r1;
+    #pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t send = h16 ? r8[j] : r8[j + 4], keep = h16 ? r8[j + 4] : r8[j];
+      r4[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+    #pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const uint32_t send = h8 ? r4[j] : r4[j + 2], keep = h8 ? r4[j + 2] : r4[j];
+      r2[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    {
+      const uint32_t send = h4 ? r2[0] : r2[1], keep = h4 ? r2[1] : r2[0];
+      r1 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    r1 += __shfl_xor_sync(0xffffffffu, r1, 2);
+    r1 += __shfl_xor_sync(0xffffffffu, r1, 1);
+    ptx::red_global_add_if(yz_col + y, r1, (lane & 3) == 0 && r1 != 0 && (lane >> 2) < g.zc);
+    add_owned<8>(pp.rows_addr + (uint32_t)(parity * RL::WORDS * 4) + 4 * (RL::XY + 8 * lane), cs);
+    __syncthreads();
+    pp.end_step(parity, col, y);
+    parity ^= 1;
+    if (++cst == STAGES) { cst = 0; cphase ^= 1u; }
+    cur.advance(p);
+  }
+  flush_zx();
+}
+
+// Oblique warps (8..15): DIAG / ANTI / X2P / X2M windows.
+template <typename T, int NI, int STAGES>
+__device__ __forceinline__ void oblique_loop(Pipe<T, NI, STAGES>& pp, int w, int lane) {
+  using RL = RowLayout<NI>;
+  const StreamParams& p = *pp.p;
+  Cursor cur;
+  cur.init(p);
+  int32_t col = -1;
+  ColGeom g;
+  g.zc = 0; g.xok = false;
+  int cst = 0, parity = 0;
+  uint32_t cphase = 0;
+  while (!cur.done) {
+    const int32_t y = cur.y();
+    if (cur.c != col) { col = cur.c; g.set(p, col, w, lane); }
+    ptx::mbar_wait(&pp.full[cst], cphase);
+    const T* tile = reinterpret_cast<const T*>(pp.stages + cst * Pipe<T, NI, STAGES>::STAGE_BYTES) + (8 * w) * SX + 8 * lane;
+    uint32_t wd[16], wa[16], wp[24], wm[24];
+    #pragma unroll
+    for (int i = 0; i < 16; ++i) { wd[i] = 0; wa[i] = 0; }
+    #pragma unroll
+    for (int i = 0; i < 24; ++i) { wp[i] = 0; wm[i] = 0; }
+    #pragma unroll
+    for (int tp = 0; tp < 4; ++tp) {
+      const int t0 = 2 * tp;
+      uint32_t a[8], bb[8];
+      load_pair<T>(tile, t0, a, bb, p.offset, g.xok, g.zc);
+      fold_pair<15>(wd, a, bb, t0, t0 + 1);
+      if (NI > DPM_IMG_ANTI) fold_pair<15>(wa, a, bb, 7 - t0, 6 - t0);
+      if (NI > DPM_IMG_X2P) fold_pair<22>(wp, a, bb, 2 * t0, 2 * t0 + 2);
+      if (NI > DPM_IMG_X2M) fold_pair<22>(wm, a, bb, 14 - 2 * t0, 12 - 2 * t0);
+    }
+    merge_owned<15>(wd, lane);
+    if (NI > DPM_IMG_ANTI) merge_owned<15>(wa, lane);
+    if (NI > DPM_IMG_X2P) merge_owned<22>(wp, lane);
+    if (NI > DPM_IMG_X2M) merge_owned<22>(wm, lane);
+    const uint32_t rp = pp.rows_addr + (uint32_t)(parity * RL::WORDS * 4);
+    {
+      const uint32_t base = rp + 4 * (RL::DG + 8 * lane + 8 * w);
+      add_owned<8>(base, wd);
+      if (lane == 31) add_spill<7>(base, wd + 8, 0);
+    }
+    if (NI > DPM_IMG_ANTI) {
+      const uint32_t base = rp + 4 * (RL::AN + 8 * lane - 8 * w + 56);
+      add_owned<8>(base, wa);
+      if (lane == 31) add_spill<7>(base, wa + 8, 0);
+    }
+    if (NI > DPM_IMG_X2P) {
+      const uint32_t base = rp + 4 * (RL::XP + 8 * lane + 16 * w);
+      add_owned<8>(base, wp);
+      if (lane >= 30) add_spill<14>(base, wp + 8, lane == 31 ? 0 : 8);
+    }
+    if (NI > DPM_IMG_X2M) {
+      const uint32_t base = rp + 4 * (RL::XM + 8 * lane - 16 * w + 112);
+      add_owned<8>(base, wm);
+      if (lane >= 30) add_spill<14>(base, wm + 8, lane == 31 ? 0 : 8);
+    }
+    __syncthreads();
+    pp.end_step(parity, col, y);
+    parity ^= 1;
+    if (++cst == STAGES) { cst = 0; cphase ^= 1u; }
+    cur.advance(p);
+  }
+}
+
+template <typename T, int NI, int STAGES>
+__global__ void __launch_bounds__(THREADS, 1)
+project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
+  using RL = RowLayout<NI>;
+  using P = Pipe<T, NI, STAGES>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  P pp;
+  pp.p = &p;
+  pp.tmap = &tmap;
+  pp.stages = smem;
+  pp.rows = reinterpret_cast<uint32_t*>(smem + STAGES * P::STAGE_BYTES);
+  pp.full = reinterpret_cast<uint64_t*>(pp.rows + 2 * RL::WORDS);
+  pp.rows_addr = ptx::smem_addr(pp.rows);
+  pp.tid = threadIdx.x;
+  pp.pst = 0;
+  const int lane = pp.tid & 31, warp = pp.tid >> 5;
+  for (int i = pp.tid; i < 2 * RL::WORDS; i += THREADS) pp.rows[i] = 0;
+  if (pp.tid == 0) {
+    ptx::prefetch_tmap(&tmap);
+    for (int i = 0; i < STAGES; ++i) ptx::mbar_init(&pp.full[i], 1);
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  if (pp.tid == 0) {
+    pp.prod.init(p);
+    for (int i = 0; i < STAGES && !pp.prod.done; ++i) pp.issue();
+  }
+  // warps 0..7: ZX / XY / YZ;  warps 8..15: obliques.  Warp w and w+8 read the same planes.
+  if (warp < 8) axis_loop<T, NI, STAGES>(pp, warp, lane);
+  else oblique_loop<T, NI, STAGES>(pp, warp - 8, lane);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+static bool stream_eligible(const dpm_volume_desc* d, const void* vox) {
+  const int64_t es = d->dtype == DPM_U8 ? 1 : 2;
+  if (d->L < 64 || d->N < 8) return false;
+  if ((d->stride_y * es) % 16 || (d->stride_z * es) % 16) return false;
+  if (d->B > 1 && (d->stride_b * es) % 16) return false;
+  if (d->L % 8) return false;  // a lane vector never straddles the row end
+  if (reinterpret_cast<uintptr_t>(vox) % 16) return false;
+  if (d->L > 0x7fffffffLL || d->M > 0x7fffffffLL || d->N > 0x7fffffffLL || d->B > 0x7fffffffLL) return false;
+  return encode_fn() != nullptr;
+}
+
 size_t project_stream_workspace(const dpm_volume_desc*, int) { return 0; }
-int launch_project_stream(const dpm_volume_desc*, const void*, const ImageSet&, void*, size_t, cudaStream_t,
-                          bool* handled) {
-  *handled = false;
+
+template <typename T> struct StageCount { static constexpr int value = sizeof(T) == 1 ? 8 : 5; };
+
+template <typename T, int NI>
+static int launch_one(const CUtensorMap& map, int grid, cudaStream_t st, const StreamParams& p) {
+  constexpr int S = StageCount<T>::value;
+  constexpr size_t bytes = (size_t)S * SZ * SX * sizeof(T) + 2 * RowLayout<NI>::WORDS * 4 + S * 8;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(project_stream_kernel<T, NI, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  });
+  project_stream_kernel<T, NI, S><<<grid, THREADS, bytes, st>>>(map, p);
   return DPM_OK;
 }
+
+template <typename T>
+static int launch_typed(int n_img, const CUtensorMap& map, int grid, cudaStream_t st, const StreamParams& p) {
+  switch (n_img) {
+    case 4: return launch_one<T, 4>(map, grid, st, p);
+    case 5: return launch_one<T, 5>(map, grid, st, p);
+    case 6: return launch_one<T, 6>(map, grid, st, p);
+    default: return launch_one<T, 7>(map, grid, st, p);
+  }
+}
+
+int launch_project_stream(const dpm_volume_desc* d, const void* vox, const ImageSet& s, void*, size_t,
+                          cudaStream_t st, bool* handled) {
+  *handled = false;
+  if (s.n_img < 4 || !stream_eligible(d, vox)) return DPM_OK;
+  const int64_t es = d->dtype == DPM_U8 ? 1 : 2;
+  CUtensorMap map;
+  const cuuint64_t dims[4] = {(cuuint64_t)d->L, (cuuint64_t)d->M, (cuuint64_t)d->N, (cuuint64_t)d->B};
+  const cuuint64_t strides[3] = {(cuuint64_t)(d->stride_y * es), (cuuint64_t)(d->stride_z * es),
+                                 (cuuint64_t)((d->B > 1 ? d->stride_b : d->stride_z * d->N) * es)};
+  const cuuint32_t box[4] = {SX, 1, SZ, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = encode_fn()(&map, d->dtype == DPM_U8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16,
+                                 4, const_cast<void*>(vox), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return DPM_OK;  // not describable by TMA: generic path
+  StreamParams p;
+  p.L = d->L; p.M = d->M; p.N = d->N; p.B = d->B; p.offset = d->offset;
+  p.ntx = (d->L + SX - 1) / SX; p.ntz = (d->N + SZ - 1) / SZ;
+  p.ncol = p.ntx * p.ntz * d->B;
+  p.s = s;
+  // y-band: keep one band's image rows (plus the YZ cells) within ~40 MB of L2
+  int64_t row_bytes = 0;
+  for (int k = 0; k < s.n_img; ++k)
+    if (k != DPM_IMG_YZ && k != DPM_IMG_ZX) row_bytes += s.W[k] * 4 * d->B;
+  row_bytes += d->N * 4 * d->B;
+  p.band = imax64(16, imin64(d->M, (40ll << 20) / imax64(row_bytes, 1)));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)imin64(sms, p.ncol * d->M);
+  switch (d->dtype) {
+    case DPM_U8: launch_typed<uint8_t>(s.n_img, map, grid, st, p); break;
+    case DPM_U16: launch_typed<uint16_t>(s.n_img, map, grid, st, p); break;
+    default: launch_typed<int16_t>(s.n_img, map, grid, st, p); break;
+  }
+  note_launches(1);
+  *handled = true;
+  DPM_CUDA_CHECK_LAUNCH();
+  return DPM_OK;
+}
+
 }  // namespace dpm

@@ -1,15 +1,18 @@
 """Quick end-to-end parity of the CUDA pipeline against the C oracle."""
 import numpy as np
 import pytest
+import torch
 
 import oracle
 import paper_2012_08099_b200 as vm
+from paper_2012_08099_b200 import engine
 
 pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("dims,bits,order", [((5, 4, 3), 8, 3), ((7, 6, 5), 16, 4), ((9, 7, 5), 8, 6),
-                                               ((64, 64, 64), 8, 3), ((33, 17, 20), 16, 6)])
+                                               ((64, 64, 64), 8, 3), ((33, 17, 20), 16, 6),
+                                               ((264, 19, 72), 16, 6), ((320, 9, 70), 8, 5)])
 def test_dpm_matches_oracle(cuda, dims, bits, order):
     v = vm.random(dims, bits, seed=3)
     got = vm.dpm_moments(v, order)
@@ -17,10 +20,25 @@ def test_dpm_matches_oracle(cuda, dims, bits, order):
     assert got.values == want
 
 
-@pytest.mark.parametrize("dims", [(1, 1, 1), (5, 3, 2), (16, 16, 16), (70, 9, 33)])
-def test_projections_match_oracle(cuda, dims):
-    v = vm.random(dims, 16, seed=1)
+@pytest.mark.parametrize("dims", [(1, 1, 1), (5, 3, 2), (16, 16, 16), (70, 9, 33), (64, 8, 8),
+                                  (256, 3, 64), (264, 5, 65), (512, 2, 130)])
+@pytest.mark.parametrize("bits", [8, 16])
+def test_projections_match_oracle(cuda, dims, bits):
+    v = vm.random(dims, bits, seed=1)
     got = vm.project_extended(v)
     want = oracle.project(v.voxels, 7)
     for k, name in enumerate(vm.projection.EXTENDED_NAMES):
         assert np.array_equal(got[name].pixels, want[k]), name
+
+
+def test_int16_offset_and_batch(cuda):
+    rng = np.random.default_rng(5)
+    vol = rng.integers(-1024, 3072, size=(3, 40, 24, 128), dtype=np.int16)
+    t = torch.from_numpy(vol).cuda()
+    res = engine.moments(t, 4, offset=1024)
+    torch.cuda.synchronize()
+    got = res.i128.cpu().numpy()
+    for b in range(3):
+        want = oracle.naive(vol[b], 4, offset=1024)
+        assert engine.i128_to_ints(got[b]) == [want[k] for k in vm.moment_indices(4)]
+    assert res.status.cpu().numpy().tolist() == [0, 0, 0]

@@ -1,0 +1,174 @@
+"""Pin the C oracle (oracle/dpm_oracle.c) to the reference before trusting it.
+
+Every check compares the oracle with outputs of the reference implementation
+recorded in tests/golden/ (tests/golden/make_golden.py), or with the
+reference's own known-answer tests restated (pkg/tests/*.py)."""
+from math import comb
+
+import numpy as np
+import pytest
+
+import oracle
+import pyoracle
+from golden_data import (ORIENTATIONS, configs, moments, parse_moments, projections, sha,
+                         volume_for)
+from paper_2012_08099_b200 import synth
+
+
+def test_oracle_projections_equal_reference_golden():
+    vols, imgs = projections()
+    assert len(vols) >= 25
+    for name, v in vols.items():
+        got = oracle.project(v, 5)
+        for k, o in enumerate(ORIENTATIONS):
+            assert np.array_equal(got[k], imgs[(name, o)]), (name, o)
+
+
+@pytest.mark.parametrize("K", [3, 4])
+def test_oracle_moments_equal_reference_golden(K):
+    for name, entry in moments().items():
+        v = volume_for(name)
+        want = parse_moments(entry[f"dpm{K}"])
+        assert want == parse_moments(entry[f"naive{K}"]), name   # reference self-consistency
+        assert oracle.dpm(v, K) == want, name
+        assert oracle.naive(v, K) == want, name
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg4_0", "cfg4_1", "cfg4_2", "cfg4_3"])
+def test_oracle_on_config_generators(name):
+    c = configs()[name]
+    if name == "cfg1":
+        v = synth.cfg1(c["params"]["seed"])
+    elif name == "cfg2":
+        v = synth.cfg2(c["params"]["seed"])
+    else:
+        v = synth.cfg4_volume_numpy(synth.cfg4_params(4, c["params"]["seed"])[c["params"]["index"]])
+    assert sha(v) == c["voxels_sha256"], "generator drifted from the golden voxels"
+    assert oracle.dpm(v, c["order"]) == parse_moments(c["dpm"])
+    imgs = oracle.project(v, 5)
+    for k, o in enumerate(ORIENTATIONS):
+        assert sha(imgs[k]) == c["images_sha256"][o], o
+
+
+def test_oracle_cfg1_naive_golden():
+    c = configs()["cfg1"]
+    assert oracle.naive(synth.cfg1(0), 3) == parse_moments(c["naive"])
+
+
+def test_oracle_cfg3_int16_offset():
+    c = configs()["cfg3"]
+    v = synth.cfg3(c["params"]["seed"])
+    assert sha(v) == c["voxels_sha256"]
+    got = oracle.dpm(v, 4, offset=c["params"]["offset"])
+    assert got == parse_moments(c["dpm"])
+    imgs = oracle.project(v, 5, offset=1024)
+    for k, o in enumerate(ORIENTATIONS):
+        assert sha(imgs[k]) == c["images_sha256"][o], o
+
+
+def test_oracle_cfg5_slab_and_generator_mirror():
+    c = configs()["cfg5_slab"]
+    p = c["params"]
+    v = synth.noise_slab_numpy(p["L"], p["M"], p["z0"], p["nz"], p["seed"])
+    assert sha(v) == c["voxels_sha256"]
+    assert oracle.dpm(v, 4) == parse_moments(c["dpm"])
+    assert oracle.naive(v, 3) == parse_moments(c["naive3"])
+
+
+# ---- restated reference known-answer tests (pkg/tests) ----------------------
+
+def test_uniform_xy_all_twos():                      # test_projection.py:17-21
+    v = np.ones((2, 2, 2), np.uint8)
+    assert np.all(oracle.project(v, 4)[0] == 2)
+
+
+def test_image_sizes():                              # test_projection.py:24-33
+    v = np.ones((2, 3, 5), np.uint8)
+    imgs = oracle.project(v, 7)
+    assert [im.shape for im in imgs] == [(3, 5), (2, 3), (5, 2), (3, 6), (3, 6), (3, 7), (3, 7)]
+    assert oracle.layout((5, 3, 2), 4)[2] == -1      # ANTI origin offset N-1 = 1
+
+
+def test_mri_diag_size():                            # test_projection.py:36-41
+    assert oracle.layout((512, 512, 230), 3)[:2] == (741, 512)
+    assert oracle.layout((512, 512, 230), 4)[:2] == (741, 512)
+
+
+def test_delta_indices():                            # test_projection.py:44-56
+    v = np.zeros((4, 4, 4), np.uint8); v[1, 0, 1] = 7
+    d = oracle.project(v, 5)[3]
+    assert np.argwhere(d).tolist() == [[0, 2]] and d[0, 2] == 7
+    v = np.zeros((4, 4, 4), np.uint8); v[3, 2, 0] = 7
+    a = oracle.project(v, 5)[4]
+    assert a[2, -3 + 3] == 7
+
+
+def test_delta_monomials_all_orders():               # test_moments3d.py:25-30, extended to K=6
+    v = np.zeros((6, 5, 4), np.uint8); v[3, 2, 1] = 5
+    for K in (3, 4, 5, 6):
+        for (p, q, r), val in oracle.dpm(v, K).items():
+            assert val == 5 * 1 ** p * 2 ** q * 3 ** r
+
+
+def test_two_voxel_by_hand():                        # test_moments3d.py:43-51
+    g = np.zeros((4, 4, 4), np.uint8); g[0, 0, 0] = 1; g[3, 2, 1] = 2
+    t = oracle.dpm(g, 4)
+    assert (t[(1, 1, 1)], t[(2, 1, 1)], t[(1, 2, 1)]) == (12, 12, 24)
+
+
+def test_uniform_2x2x2():                            # test_moments3d.py:33-40
+    t = oracle.dpm(np.ones((2, 2, 2), np.uint8), 4)
+    assert t[(0, 0, 0)] == 8 and t[(1, 0, 0)] == t[(0, 1, 0)] == t[(0, 0, 1)] == 4
+    assert t[(1, 1, 0)] == 2 and t[(1, 1, 1)] == 1
+
+
+def test_mixed_formula_regression():                 # test_moments3d.py:116-147
+    for seed in range(5):
+        v = np.random.default_rng(seed).integers(0, 256, (5, 7, 9), dtype=np.uint8)
+        truth = oracle.naive(v, 4)
+        imgs = oracle.project(v, 5)
+        n = v.shape[0]
+        dm = oracle.moments2d(imgs[3], 4)
+        am = oracle.moments2d(imgs[4], 4, ai=-(n - 1))
+        assert (dm[(3, 1)] - am[(3, 1)] - 2 * truth[(0, 1, 3)]) == 6 * truth[(2, 1, 1)]
+        assert (dm[(3, 1)] + am[(3, 1)] - 2 * truth[(3, 1, 0)]) == 6 * truth[(1, 1, 2)]
+
+
+@pytest.mark.parametrize("K", [3, 4, 5, 6])
+def test_order_extension_against_loop_oracle(K):
+    """Orders 5-6 are unpinned by the reference: pin them to the restated
+    conftest.oracle_moments_3d triple loop (any order) and to the direct sum."""
+    for seed, dims in enumerate([(3, 4, 5), (5, 2, 3), (1, 6, 2)]):
+        v = np.random.default_rng(seed).integers(0, 65536, dims, dtype=np.uint16)
+        want = pyoracle.moments_3d(v, K)
+        assert oracle.naive(v, K) == want
+        assert oracle.dpm(v, K) == want
+
+
+def test_extended_images_against_loop_oracle():
+    v = np.random.default_rng(4).integers(0, 256, (4, 3, 5), dtype=np.uint8)
+    imgs = oracle.project(v, 7)
+    for k, name in enumerate(("xy", "yz", "zx", "diag", "anti", "x2p", "x2m")):
+        assert np.array_equal(imgs[k], pyoracle.project(v, name)), name
+
+
+def test_slab_composition_global_coordinates():
+    """Per-slab DPM in global coordinates sums to the whole-volume moments
+    (the multi-GPU z-slab contract)."""
+    v = np.random.default_rng(9).integers(0, 65536, (17, 6, 11), dtype=np.uint16)
+    for K in (4, 6):
+        whole = oracle.dpm(v, K)
+        total = {k: 0 for k in whole}
+        for z0, z1 in ((0, 5), (5, 12), (12, 17)):
+            part = oracle.dpm(np.ascontiguousarray(v[z0:z1]), K, z0=z0)
+            for k in total:
+                total[k] += part[k]
+        assert total == whole
+
+
+def test_translation_binomial_anchor():              # test_moments3d.py:105-113
+    a = np.zeros((4, 4, 6), np.uint8); a[1, 1, 2] = 3
+    b = np.zeros((4, 4, 6), np.uint8); b[1, 1, 3] = 3
+    t0, t1 = oracle.dpm(a, 6), oracle.dpm(b, 6)
+    for p in range(7):
+        assert t1[(p, 0, 0)] == sum(comb(p, s) * t0[(s, 0, 0)] for s in range(p + 1))
