@@ -318,3 +318,52 @@ void vmo_set_threads(int n) {
   (void)n;
 #endif
 }
+
+/* ---- host copy of the config-5 synthetic volume generator ------------------
+ * Same integer formula as paper_2012_08099_b200/csrc/synth.cu (value noise,
+ * 4 octaves, quantised smoothstep weights), so CPU baselines and checks can
+ * build bounded samples of the cfg5 volume without a GPU. */
+static inline uint64_t vmo_mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static inline uint64_t vmo_lattice(uint64_t seed, int o, int64_t cx, int64_t cy, int64_t cz) {
+  uint64_t h = seed ^ ((uint64_t)o << 56);
+  h = vmo_mix64(h ^ ((uint64_t)cx * 0x8CB92BA72F3D8DD7ull));
+  h = vmo_mix64(h ^ ((uint64_t)cy * 0xA24BAED4963EE407ull));
+  h = vmo_mix64(h ^ ((uint64_t)cz * 0x9FB21C651E98DF25ull));
+  return h >> 48;
+}
+static inline uint64_t vmo_sweight(int64_t f, int64_t S) {
+  return (uint64_t)((f * f * (3 * S - 2 * f)) * 65536 / (S * S * S));
+}
+void vmo_synth_noise_u16(uint16_t* out, int64_t L, int64_t M, int64_t z0, int64_t nz, uint64_t seed) {
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int64_t zi = 0; zi < nz; ++zi) {
+    for (int64_t y = 0; y < M; ++y) {
+      const int64_t z = z0 + zi;
+      for (int64_t x = 0; x < L; ++x) {
+        uint64_t sum = 0;
+        for (int o = 0; o < 4; ++o) {
+          const int64_t S = 128 >> o;
+          const int64_t cx = x / S, cy = y / S, cz = z / S;
+          const uint64_t wx = vmo_sweight(x - cx * S, S), wy = vmo_sweight(y - cy * S, S), wz = vmo_sweight(z - cz * S, S);
+          uint64_t c[2];
+          for (int dz = 0; dz < 2; ++dz) {
+            uint64_t b[2];
+            for (int dy = 0; dy < 2; ++dy) {
+              const uint64_t h0 = vmo_lattice(seed, o, cx, cy + dy, cz + dz);
+              const uint64_t h1 = vmo_lattice(seed, o, cx + 1, cy + dy, cz + dz);
+              b[dy] = h0 * (65536 - wx) + h1 * wx;
+            }
+            c[dz] = b[0] * (65536 - wy) + b[1] * wy;
+          }
+          sum += ((c[0] * (65536 - wz) + c[1] * wz) >> 48) << (3 - o);
+        }
+        out[(zi * M + y) * L + x] = (uint16_t)(sum / 15);
+      }
+    }
+  }
+}

@@ -46,6 +46,7 @@ def load() -> ctypes.CDLL:
     lib.vmo_dpm.restype = ctypes.c_int
     lib.vmo_naive.argtypes = [vp, ctypes.c_int, i32, i64, i64, i64, i64, ctypes.c_int, vp]
     lib.vmo_set_threads.argtypes = [ctypes.c_int]
+    lib.vmo_synth_noise_u16.argtypes = [vp, i64, i64, i64, i64, ctypes.c_uint64]
     return lib
 
 
@@ -151,3 +152,10 @@ def naive(voxels: np.ndarray, order: int, z0: int = 0, offset: int = 0) -> dict[
     out = np.zeros((len(moment_indices(order)), 2), dtype=np.int64)
     load().vmo_naive(v.ctypes.data, code, offset, *dims, z0, order, out.ctypes.data)
     return dict(zip(moment_indices(order), _from_i128(out)))
+
+
+def synth_noise(L: int, M: int, z0: int, nz: int, seed: int) -> np.ndarray:
+    """[nz, M, L] uint16 slab of the config-5 noise volume (host copy of csrc/synth.cu)."""
+    out = np.empty((nz, M, L), dtype=np.uint16)
+    load().vmo_synth_noise_u16(out.ctypes.data, L, M, z0, nz, seed & ((1 << 64) - 1))
+    return out

@@ -150,20 +150,28 @@ def moments(vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0, n_globa
     return out
 
 
-def moments2d_partial(vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0,
-                      stream: torch.cuda.Stream | None = None) -> torch.Tensor:
-    """Project + exact 2D moments of a slab in GLOBAL coordinates; returns the
-    limb accumulator [B, n_img, n2d, 4] (int64 storage of uint64 sums).  Limb
-    accumulators of z-slabs add elementwise (moments are linear in voxels)."""
-    check_order(order)
-    n_img = num_images(order)
-    imgs = project(vox, n_img, offset, z0, stream)
+def moments2d_images(vox: torch.Tensor, imgs: list[torch.Tensor], order: int, offset: int = 0, z0: int = 0,
+                     stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Exact 2D moments (global coordinates) of images made by ``project`` from
+    ``vox``; returns the limb accumulator [B, n_img, n2d, 4] (int64 storage of
+    uint64 sums)."""
     desc = make_desc(vox, offset, z0)
+    n_img = len(imgs)
     acc = torch.empty((desc.B, n_img, n2d(order), 4), dtype=torch.int64, device=vox.device)
     ptrs = (ctypes.c_void_p * n_img)(*[t.data_ptr() for t in imgs])
     nat.check(nat.lib().dpm_moments2d(ctypes.byref(desc), n_img, ptrs, order, acc.data_ptr(),
                                       stream_handle(stream)), "dpm_moments2d")
     return acc
+
+
+def moments2d_partial(vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0,
+                      stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Project + exact 2D moments of a slab in GLOBAL coordinates; returns the
+    limb accumulator [B, n_img, n2d, 4].  Limb accumulators of z-slabs add
+    elementwise (moments are linear in the voxels)."""
+    check_order(order)
+    imgs = project(vox, num_images(order), offset, z0, stream)
+    return moments2d_images(vox, imgs, order, offset, z0, stream)
 
 
 def derive(acc: torch.Tensor, order: int, stream: torch.cuda.Stream | None = None) -> DeviceMoments:
@@ -211,3 +219,10 @@ def synth_noise(L: int, M: int, z0: int, n_planes: int, seed: int, device=None,
     nat.check(nat.lib().dpm_synth_noise_u16(out.data_ptr(), L, M, z0, n_planes, seed & ((1 << 64) - 1),
                                             stream_handle(stream)), "dpm_synth_noise_u16")
     return out
+
+
+def acc_add(out: torch.Tensor, inp: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:
+    """out += inp for limb accumulators, on the device (dpm_acc_add kernel)."""
+    assert out.shape == inp.shape and out.dtype == torch.int64 == inp.dtype
+    nat.check(nat.lib().dpm_acc_add(out.data_ptr(), inp.data_ptr(), out.numel(), stream_handle(stream)),
+              "dpm_acc_add")

@@ -187,7 +187,41 @@ def _sweight(f: np.ndarray, S: int) -> np.ndarray:
 
 
 def noise_slab_numpy(L: int, M: int, z0: int, nz: int, seed: int) -> np.ndarray:
-    """Host mirror of dpm_synth_noise_u16: [nz, M, L] uint16, planes z0..z0+nz-1."""
+    """Host mirror of dpm_synth_noise_u16: [nz, M, L] uint16, planes z0..z0+nz-1.
+
+    Separable evaluation of the same integer formula: the x-lerp is done once
+    per lattice row, then rows are gathered per y (bit-identical to the
+    per-voxel form ``noise_slab_numpy_direct``)."""
+    out = np.empty((nz, M, L), dtype=np.uint16)
+    one = np.uint64(65536)
+    xs = np.arange(L, dtype=np.int64)
+    ys = np.arange(M, dtype=np.int64)
+    with np.errstate(over="ignore"):
+        for zi in range(nz):
+            z = z0 + zi
+            total = np.zeros((M, L), dtype=np.uint64)
+            for o in range(4):
+                S = 128 >> o
+                cx, cy, cz = xs // S, ys // S, z // S
+                wx = _sweight(xs - cx * S, S)[None, :]
+                wy = _sweight(ys - cy * S, S)[:, None]
+                wz = _sweight(np.array([z - cz * S]), S)[0]
+                ncy, ncx = int(cy.max()) + 2, int(cx.max()) + 2
+                rows = np.arange(ncy, dtype=np.int64)[:, None]
+                cols = np.arange(ncx, dtype=np.int64)[None, :]
+                c = []
+                for dz in (0, 1):
+                    H = _lattice(seed, o, cols, rows, np.full((ncy, ncx), cz + dz, dtype=np.int64))  # [ncy, ncx]
+                    B = H[:, cx] * (one - wx) + H[:, cx + 1] * wx       # [ncy, L], < 2^32
+                    c.append(B[cy] * (one - wy) + B[cy + 1] * wy)      # [M, L],  < 2^48
+                v = (c[0] * (one - wz) + c[1] * wz) >> np.uint64(48)
+                total += v << np.uint64(3 - o)
+            out[zi] = (total // np.uint64(15)).astype(np.uint16)
+    return out
+
+
+def noise_slab_numpy_direct(L: int, M: int, z0: int, nz: int, seed: int) -> np.ndarray:
+    """Per-voxel form of the noise (slow; cross-checks the separable form)."""
     z, y, x = np.meshgrid(np.arange(z0, z0 + nz, dtype=np.int64), np.arange(M, dtype=np.int64),
                           np.arange(L, dtype=np.int64), indexing="ij")
     total = np.zeros(z.shape, dtype=np.uint64)
