@@ -226,3 +226,15 @@ def acc_add(out: torch.Tensor, inp: torch.Tensor, stream: torch.cuda.Stream | No
     assert out.shape == inp.shape and out.dtype == torch.int64 == inp.dtype
     nat.check(nat.lib().dpm_acc_add(out.data_ptr(), inp.data_ptr(), out.numel(), stream_handle(stream)),
               "dpm_acc_add")
+
+
+def ints_to_limbs(values) -> np.ndarray:
+    """Exact ints -> the limb-accumulator encoding [..., 4] (int64 storage of
+    uint64 limb sums: value = sum_k limb_k 2^(32k) mod 2^128)."""
+    arr = np.asarray(values, dtype=object)
+    out = np.zeros(arr.shape + (4,), dtype=np.uint64)
+    for idx, v in np.ndenumerate(arr):
+        u = int(v) % (1 << 128)
+        for k in range(4):
+            out[idx + (k,)] = (u >> (32 * k)) & 0xFFFFFFFF
+    return out.view(np.int64)

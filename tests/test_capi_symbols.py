@@ -1,0 +1,69 @@
+"""The C-ABI library loads (no GPU needed) and exports exactly what include/dpm_b200.h declares."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2012_08099_b200 import _native as nat
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "dpm_b200.h")
+
+
+def declared():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"DPM_API\s+[\w\s\*]+?\b(dpm_\w+)\s*\(", txt)))
+
+
+def test_header_declares_the_exported_list():
+    assert declared() == sorted(nat.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = nat.lib()
+    for name in declared():
+        assert getattr(lib, name) is not None, name
+
+
+def test_host_only_entry_points():
+    lib = nat.lib()
+    assert [lib.dpm_num_images(k) for k in (3, 4, 5, 6)] == [4, 5, 6, 7]
+    assert lib.dpm_num_images(2) == 0 and lib.dpm_num_images(7) == 0
+    assert [lib.dpm_num_moments3d(k) for k in (3, 4, 6)] == [20, 35, 84]
+    assert lib.dpm_strerror(nat.DPM_EINVAL).decode() == "invalid argument"
+    assert lib.dpm_check_envelope(2048, 2048, 2048, 65535, 6) == nat.DPM_OK
+    assert lib.dpm_check_envelope(65536, 65536, 65536, 65535, 6) == nat.DPM_EOVERFLOW
+    assert lib.dpm_check_envelope(0, 1, 1, 1, 3) == nat.DPM_EINVAL
+
+
+@pytest.mark.parametrize("dims,z0", [((5, 3, 2), 0), ((512, 512, 230), 0), ((7, 9, 11), 13), ((2048, 2048, 256), 1024)])
+def test_image_layout_matches_oracle(dims, z0):
+    d = nat.VolumeDesc()
+    d.L, d.M, d.N = dims
+    d.B = 1
+    d.z0 = z0
+    for img in range(7):
+        out = [ctypes.c_int64() for _ in range(4)]
+        assert nat.lib().dpm_image_layout(ctypes.byref(d), img, *[ctypes.byref(o) for o in out]) == 0
+        assert tuple(o.value for o in out) == oracle.layout(dims, img, z0)
+
+
+def test_invalid_arguments_rejected_without_a_device():
+    d = nat.VolumeDesc()
+    d.L = d.M = d.N = 4
+    d.B = 1
+    d.stride_y, d.stride_z, d.stride_b = 4, 16, 64
+    d.dtype = 9   # unsupported dtype
+    imgs = (ctypes.c_void_p * 4)()
+    assert nat.lib().dpm_project(ctypes.byref(d), None, 4, imgs, None, 0, None) == nat.DPM_EINVAL
+    d.dtype = nat.DPM_U16
+    d.L = 70000   # longest ray * 65535 would overflow a uint32 ray sum
+    d.stride_y, d.stride_z = 70000, 280000
+    assert nat.lib().dpm_project(ctypes.byref(d), None, 4, imgs, None, 0, None) == nat.DPM_EOVERFLOW
+    with pytest.raises(ValueError):
+        nat.check(nat.DPM_EINVAL, "x")
+    with pytest.raises(OverflowError):
+        nat.check(nat.DPM_EOVERFLOW, "x")
+    assert np.int64  # numpy import used

@@ -1,0 +1,186 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+outputs (tests/golden/, generated from /root/reference) and the C oracle.
+
+Projections are bit-exact; moments are exact integers (the reference returns
+exact Python ints; our fp64 copies are therefore within 1 ulp)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import pyoracle
+import paper_2012_08099_b200 as vm
+from golden_data import (ORIENTATIONS, configs, moments, parse_moments, projections, sha,
+                         volume_for)
+from paper_2012_08099_b200 import engine, synth
+from paper_2012_08099_b200.errors import InconsistencyError
+
+pytestmark = pytest.mark.gpu
+
+
+def _ints(res, b=0):
+    return engine.i128_to_ints(res.i128[b].cpu().numpy())
+
+
+def test_golden_projections_bit_exact(cuda):
+    vols, imgs = projections()
+    for name, v in vols.items():
+        ps = vm.project_all(vm.Volume(v.copy()))
+        for o in vm.Orientation:
+            assert np.array_equal(ps[o].pixels, imgs[(name, o.value)]), (name, o)
+        assert ps.anti.origin_offset == v.shape[0] - 1
+
+
+@pytest.mark.parametrize("K", [3, 4])
+def test_golden_moments_exact(cuda, K):
+    for name, entry in moments().items():
+        v = volume_for(name)
+        got = vm.dpm_moments(vm.Volume(v.copy()), K)
+        assert got.values == parse_moments(entry[f"dpm{K}"]), name
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4_0", "cfg4_1", "cfg4_2", "cfg4_3", "cfg5_slab"])
+def test_golden_configs(cuda, name):
+    c = configs()[name]
+    p = c["params"]
+    off = p.get("offset", 0)
+    if name == "cfg1":
+        v = synth.cfg1(p["seed"])
+    elif name == "cfg2":
+        v = synth.cfg2(p["seed"])
+    elif name == "cfg3":
+        v = synth.cfg3(p["seed"])
+    elif name.startswith("cfg4"):
+        v = synth.cfg4_volume_numpy(synth.cfg4_params(4, p["seed"])[p["index"]])
+    else:
+        v = engine.synth_noise(p["L"], p["M"], p["z0"], p["nz"], p["seed"]).cpu().numpy()
+    assert sha(v) == c["voxels_sha256"]
+    t = torch.from_numpy(v).cuda()
+    res = engine.moments(t, c["order"], offset=off)
+    torch.cuda.synchronize()
+    assert int(res.status[0]) == 0
+    want = parse_moments(c["dpm"])
+    assert dict(zip(vm.moment_indices(c["order"]), _ints(res))) == want
+    f64 = res.f64[0].cpu().numpy()
+    exact = np.array([float(want[k]) for k in vm.moment_indices(c["order"])])
+    assert np.all(np.abs(f64 - exact) <= 1e-12 * np.maximum(np.abs(exact), 1.0))
+    imgs = engine.project(t, 5, offset=off)
+    torch.cuda.synchronize()
+    for k, o in enumerate(ORIENTATIONS):
+        px = imgs[k][0].cpu().numpy().view(np.uint32).astype(np.int64)
+        assert sha(px) == c["images_sha256"][o], o
+
+
+@pytest.mark.parametrize("K", [5, 6])
+def test_orders_5_6_against_loop_oracle(cuda, K):
+    for seed, dims in enumerate([(5, 4, 3), (2, 6, 5), (7, 1, 4), (1, 1, 1)]):
+        v = vm.random(dims, 16, seed=seed)
+        assert vm.dpm_moments(v, K).values == pyoracle.moments_3d(v.voxels, K)
+
+
+def test_known_answers(cuda):
+    v = vm.delta((4, 5, 6), (1, 2, 3), 5)                      # test_moments3d.py:25-30
+    for K in (3, 4, 5, 6):
+        for (p, q, r), val in vm.dpm_moments(v, K).items():
+            assert val == 5 * 1 ** p * 2 ** q * 3 ** r
+    t = vm.dpm_moments(vm.uniform((2, 2, 2), 1), 4)          # :33-40
+    assert (t.mass, t[(1, 0, 0)], t[(1, 1, 0)], t[(1, 1, 1)]) == (8, 4, 2, 1)
+    g = np.zeros((4, 4, 4), np.uint8); g[0, 0, 0] = 1; g[3, 2, 1] = 2    # :43-51
+    t = vm.dpm_moments(vm.Volume(g), 4)
+    assert (t[(1, 1, 1)], t[(2, 1, 1)], t[(1, 2, 1)]) == (12, 12, 24)
+    img = vm.project(vm.delta((4, 4, 4), (1, 0, 1), 7), vm.Orientation.DIAG)   # test_projection.py:44-49
+    assert np.argwhere(img.pixels).tolist() == [[0, 2]] and img.pixels[0, 2] == 7
+    img = vm.project(vm.delta((4, 4, 4), (0, 2, 3), 7), vm.Orientation.ANTI)   # :52-56
+    assert img.origin_offset == 3 and img.pixels[2, 0] == 7
+    ps = vm.project_all(vm.Volume(np.zeros((230, 512, 512), np.uint8)))        # :36-41
+    assert (ps.diag.width, ps.diag.height) == (741, 512) and (ps.anti.width, ps.anti.height) == (741, 512)
+
+
+def test_mixed_formula_regression_on_device_images(cuda):
+    """test_moments3d.py:116-147 restated: the +-45 degree recombination pinned
+    on the device images (oracle 2D moments as the checker)."""
+    for seed in range(5):
+        v = vm.random((9, 7, 5), 8, seed)
+        truth = oracle.naive(v.voxels, 4)
+        ps = vm.project_all(v)
+        dm = oracle.moments2d(ps.diag.pixels, 4)
+        am = oracle.moments2d(ps.anti.pixels, 4, ai=-ps.anti.origin_offset)
+        assert dm[(3, 1)] - am[(3, 1)] - 2 * truth[(0, 1, 3)] == 6 * truth[(2, 1, 1)]
+        assert dm[(3, 1)] + am[(3, 1)] - 2 * truth[(3, 1, 0)] == 6 * truth[(1, 1, 2)]
+
+
+def test_engine_equivalence_and_invariants(cuda):
+    for seed in range(3):                                     # test_moments3d.py:54-72
+        v = vm.random((12, 9, 15), 16, seed)
+        assert vm.dpm_moments(v, 4).values == oracle.naive(v.voxels, 4)
+    a, b = vm.random((5, 6, 7), 8, 1), vm.random((5, 6, 7), 8, 2)            # linearity :96-102
+    s = vm.Volume((a.voxels.astype(np.uint16) + b.voxels).astype(np.uint16))
+    ta, tb, ts = (vm.dpm_moments(x, 6) for x in (a, b, s))
+    assert all(ts[k] == ta[k] + tb[k] for k in ts.values)
+    v = vm.random((6, 5, 4), 8, seed=3)                       # relabel :88-93
+    vp = vm.Volume(np.ascontiguousarray(v.voxels.transpose(2, 0, 1)))
+    t, tp = vm.dpm_moments(v, 6), vm.dpm_moments(vp, 6)
+    assert all(val == t[(r, p, q)] for (p, q, r), val in tp.items())
+
+
+def test_overflow_envelope_and_order_errors(cuda):
+    v = vm.random((3, 200, 200), 16, seed=0)                  # :234-237 tall-thin 16-bit
+    assert vm.dpm_moments(v, 4).values == oracle.naive(v.voxels, 4)
+    with pytest.raises(ValueError, match="order"):
+        vm.dpm_moments(vm.uniform((2, 2, 2), 1), 7)
+
+
+def test_inconsistency_detected_on_corrupted_image(cuda):
+    """test_moments3d.py:168-184 restated on the device pipeline: a projection
+    route that disagrees must raise InconsistencyError naming the disagreement."""
+    v = torch.from_numpy(vm.random((8, 8, 8), 8, seed=1).voxels.copy()).cuda()
+    imgs = engine.project(v, 5)
+    imgs[0][0, 0, 0] += 1
+    acc = engine.moments2d_images(v, imgs, 4)
+    res = engine.derive(acc, 4)
+    torch.cuda.synchronize()
+    from paper_2012_08099_b200.moments3d import raise_status
+    with pytest.raises(InconsistencyError, match="disagree"):
+        raise_status(int(res.status[0]))
+
+
+def test_batch_and_streaming_match_resident(cuda):
+    rng = np.random.default_rng(7)
+    batch = rng.integers(0, 256, size=(5, 24, 16, 64), dtype=np.uint8)
+    got = vm.dpm_moments_batch(batch, 6)
+    for b in range(5):
+        assert got[b].values == oracle.naive(batch[b], 6)
+    from paper_2012_08099_b200.streaming import HostStreamer
+    vol = torch.from_numpy(rng.integers(0, 65536, size=(100, 40, 72), dtype=np.uint16)).pin_memory()
+    hs = HostStreamer(tuple(vol.shape), vol.dtype, 6, chunk_planes=16)
+    res = hs.moments(vol)
+    torch.cuda.synchronize()
+    assert dict(zip(vm.moment_indices(6), _ints(res))) == oracle.naive(vol.numpy(), 6)
+
+
+def test_zslab_composition_on_device(cuda):
+    vol = engine.synth_noise(512, 96, 0, 200, 3)
+    whole = _ints(engine.moments(vol, 6))
+    for splits in ((0, 200), (0, 64, 200), (0, 7, 100, 129, 200)):
+        acc = None
+        for z0, z1 in zip(splits, splits[1:]):
+            part = engine.moments2d_partial(vol[z0:z1], 6, z0=z0)
+            if acc is None:
+                acc = part
+            else:
+                engine.acc_add(acc, part)
+        assert _ints(engine.derive(acc, 6)) == whole, splits
+
+
+def test_cfg5_full_volume_exact(cuda):
+    """The headline config at full size: 2048^3 uint16, order 6, against the
+    oracle on the same bytes, plus image-mass consistency."""
+    vol = engine.synth_noise(2048, 2048, 0, 2048, 5)
+    res = engine.moments(vol, 6)
+    torch.cuda.synchronize()
+    assert int(res.status[0]) == 0
+    host = vol.cpu().numpy()
+    oracle.set_threads(oracle.max_threads())
+    want = oracle.dpm(host, 6)
+    assert dict(zip(vm.moment_indices(6), _ints(res))) == want
+    assert want[(0, 0, 0)] == int(host.sum(dtype=np.uint64))
