@@ -122,19 +122,22 @@ __device__ __forceinline__ void merge_owned(uint32_t* win, int lane) {
   }
 }
 
-template <int NW>
+// owned cells 8g..8g+7 of a transposed region with stride S: word (c*S + g);
+// `addr` = region byte address + 4*g
+template <int S>
 __device__ __forceinline__ void add_owned(uint32_t addr, const uint32_t* win) {
-  ptx::red_shared_add<0>(addr, win[0]);  ptx::red_shared_add<4>(addr, win[1]);
-  ptx::red_shared_add<8>(addr, win[2]);  ptx::red_shared_add<12>(addr, win[3]);
-  ptx::red_shared_add<16>(addr, win[4]); ptx::red_shared_add<20>(addr, win[5]);
-  ptx::red_shared_add<24>(addr, win[6]); ptx::red_shared_add<28>(addr, win[7]);
+  ptx::red_shared_add<0 * S * 4>(addr, win[0]); ptx::red_shared_add<1 * S * 4>(addr, win[1]);
+  ptx::red_shared_add<2 * S * 4>(addr, win[2]); ptx::red_shared_add<3 * S * 4>(addr, win[3]);
+  ptx::red_shared_add<4 * S * 4>(addr, win[4]); ptx::red_shared_add<5 * S * 4>(addr, win[5]);
+  ptx::red_shared_add<6 * S * 4>(addr, win[6]); ptx::red_shared_add<7 * S * 4>(addr, win[7]);
 }
 
-template <int NS>
+// window cells 8+c (c < NS) of group g = cells of group g + 1 + c/8, slot c % 8
+template <int S, int NS>
 __device__ __forceinline__ void add_spill(uint32_t addr, const uint32_t* spill, int first) {
   #pragma unroll
   for (int c = 0; c < NS; ++c)
-    if (c >= first) ptx::red_shared_add_dyn(addr + 32 + 4 * c, spill[c]);
+    if (c >= first) ptx::red_shared_add_dyn(addr + 4 * ((c & 7) * S + 1 + (c >> 3)), spill[c]);
 }
 
 // Per-CTA cursor over its row-steps: bands in order; inside a band the CTA's
@@ -162,12 +165,25 @@ struct Cursor {
   __device__ __forceinline__ int32_t y() const { return y0 + yoff; }
 };
 
-// CTA-row regions (words) for one parity: XY | DIAG | ANTI | X2P | X2M
+// CTA-row regions for one parity, in a TRANSPOSED layout: cell i of a region
+// lives at word (i % 8) * S + i / 8 with S = 4 (mod 32).  A lane's 8 owned
+// cells are 8i'..8i'+7 with i' = lane + const, so one red.shared instruction
+// (fixed i % 8) hits 32 consecutive words -> no bank conflicts; a warp reading
+// 32 consecutive cells for the flush hits banks 4(i%8) + i/8 -> distinct too.
 template <int NI> struct RowLayout {
-  static constexpr int XY = 0, DG = SX, AN = SX + W1P, XP = SX + 2 * W1P, XM = SX + 2 * W1P + W2P;
-  static constexpr int WORDS = NI <= 4 ? SX + W1P : NI == 5 ? SX + 2 * W1P : NI == 6 ? SX + 2 * W1P + W2P
-                                                                                   : SX + 2 * W1P + 2 * W2P;
+  static constexpr int SXY = 36, SOB = 68;          // >= groups (32 / 48), = 4 mod 32
+  static constexpr int XY = 0, DG = 8 * SXY, AN = DG + 8 * SOB, XP = AN + 8 * SOB, XM = XP + 8 * SOB;
+  static constexpr int WORDS = NI <= 4 ? DG + 8 * SOB : NI == 5 ? AN + 8 * SOB : NI == 6 ? XP + 8 * SOB : XM + 8 * SOB;
+  __device__ static constexpr int addr(int region_base, int stride, int cell) { return region_base + (cell & 7) * stride + (cell >> 3); }
 };
+
+// 8-value sum as four 3-input adds
+__device__ __forceinline__ uint32_t sum8(const uint32_t* v) {
+  const uint32_t s0 = v[0] + v[1] + v[2];
+  const uint32_t s1 = s0 + v[3] + v[4];
+  const uint32_t s2 = s1 + v[5] + v[6];
+  return s2 + v[7];
+}
 
 template <typename T>
 __device__ __forceinline__ void load_pair(const T* tile, int t0, uint32_t* a, uint32_t* bb, int32_t off, bool xok, int zc) {
@@ -193,7 +209,7 @@ struct Pipe {
   uint8_t* stages;
   uint32_t* rows;
   uint64_t* full;
-  uint32_t rows_addr;
+  uint32_t rows_addr, full_addr;
   int tid;
   Cursor prod;   // producer (thread 0)
   int pst;
@@ -209,48 +225,31 @@ struct Pipe {
   }
 
   // after the row-step barrier: refill the consumed stage, flush the CTA rows (4 cells per thread-op)
-  __device__ __forceinline__ void end_step(int parity, int32_t col, int32_t y) {
+  __device__ __forceinline__ void end_step(int parity, int32_t b, int64_t X0, int64_t Z0, int32_t y) {
     if (tid == 0 && !prod.done) issue();
-    const int32_t per = (int32_t)(p->ntz * p->ntx);
-    const int32_t b = col / per, r = col - b * per;
-    const int64_t Z0 = (int64_t)(r / (int32_t)p->ntx) * SZ, X0 = (int64_t)(r % (int32_t)p->ntx) * SX;
     uint32_t* rw = rows + parity * RL::WORDS;
     const int64_t rowid = (int64_t)b * p->M + y;
-    #pragma unroll
-    for (int j = 0; j < (RL::WORDS / 4 + THREADS - 1) / THREADS; ++j) {
-      const int f = 4 * (tid + j * THREADS);
-      if (f < RL::WORDS) {
-        const uint4 v4 = *reinterpret_cast<uint4*>(rw + f);
-        *reinterpret_cast<uint4*>(rw + f) = make_uint4(0, 0, 0, 0);
-        int i, rlo = 0, rhi;
-        int64_t g0;
-        uint32_t* g;
-        if (f < RL::DG) {
-          i = f; g0 = X0; rhi = (int)imin64(SX, p->L - X0);
-          g = p->s.img[DPM_IMG_XY] + rowid * p->L;
-        } else if (f < RL::AN) {
-          const int64_t W = p->s.W[DPM_IMG_DIAG];
-          i = f - RL::DG; g0 = X0 + Z0; rhi = (int)imin64(W1, W - g0);
-          g = p->s.img[DPM_IMG_DIAG] + rowid * W;
-        } else if (NI <= DPM_IMG_X2P || f < RL::XP) {
-          const int64_t W = p->s.W[DPM_IMG_ANTI];
-          i = f - RL::AN; g0 = X0 - Z0 - 63 + p->N - 1; rlo = (int)imax64(0, -g0); rhi = (int)imin64(W1, W - g0);
-          g = p->s.img[DPM_IMG_ANTI] + rowid * W;
-        } else if (NI <= DPM_IMG_X2M || f < RL::XM) {
-          const int64_t W = p->s.W[DPM_IMG_X2P];
-          i = f - RL::XP; g0 = X0 + 2 * Z0; rhi = (int)imin64(W2, W - g0);
-          g = p->s.img[DPM_IMG_X2P] + rowid * W;
-        } else {
-          const int64_t W = p->s.W[DPM_IMG_X2M];
-          i = f - RL::XM; g0 = X0 - 2 * Z0 - 126 + 2 * (p->N - 1); rlo = (int)imax64(0, -g0); rhi = (int)imin64(W2, W - g0);
-          g = p->s.img[DPM_IMG_X2M] + rowid * W;
-        }
-        uint32_t* gp = g + g0 + i;
-        ptx::red_global_add_if(gp + 0, v4.x, v4.x != 0 && i + 0 >= rlo && i + 0 < rhi);
-        ptx::red_global_add_if(gp + 1, v4.y, v4.y != 0 && i + 1 >= rlo && i + 1 < rhi);
-        ptx::red_global_add_if(gp + 2, v4.z, v4.z != 0 && i + 2 >= rlo && i + 2 < rhi);
-        ptx::red_global_add_if(gp + 3, v4.w, v4.w != 0 && i + 3 >= rlo && i + 3 < rhi);
+    auto flush_region = [&](int base, int stride, int ncell, uint32_t* grow, int64_t g0, int64_t W) {
+      for (int i = tid; i < ncell; i += THREADS) {
+        uint32_t* cellp = rw + base + (i & 7) * stride + (i >> 3);
+        const uint32_t v = *cellp;
+        *cellp = 0;
+        const int64_t gi = g0 + i;
+        ptx::red_global_add_if(grow + gi, v, v != 0 && gi >= 0 && gi < W);
       }
+    };
+    flush_region(RL::XY, RL::SXY, SX, p->s.img[DPM_IMG_XY] + rowid * p->L, X0, p->L);
+    {
+      const int64_t W = p->s.W[DPM_IMG_DIAG];
+      flush_region(RL::DG, RL::SOB, W1, p->s.img[DPM_IMG_DIAG] + rowid * W, X0 + Z0, W);
+      if (NI > DPM_IMG_ANTI)
+        flush_region(RL::AN, RL::SOB, W1, p->s.img[DPM_IMG_ANTI] + rowid * W, X0 - Z0 - 63 + p->N - 1, W);
+    }
+    if (NI > DPM_IMG_X2P) {
+      const int64_t W = p->s.W[DPM_IMG_X2P];
+      flush_region(RL::XP, RL::SOB, W2, p->s.img[DPM_IMG_X2P] + rowid * W, X0 + 2 * Z0, W);
+      if (NI > DPM_IMG_X2M)
+        flush_region(RL::XM, RL::SOB, W2, p->s.img[DPM_IMG_X2M] + rowid * W, X0 - 2 * Z0 - 126 + 2 * (p->N - 1), W);
     }
   }
 };
@@ -309,7 +308,7 @@ __device__ __forceinline__ void axis_loop(Pipe<T, NI, STAGES>& pp, int w, int la
       zx_col = p.s.img[DPM_IMG_ZX] + (int64_t)g.b * p.L * p.N + (g.X0 + 8 * lane) * p.N + g.Z0 + 8 * w;
       yz_col = p.s.img[DPM_IMG_YZ] + (int64_t)g.b * p.M * p.N + (g.Z0 + 8 * w + (lane >> 2)) * p.M;
     }
-    ptx::mbar_wait(&pp.full[cst], cphase);
+    ptx::mbar_wait_addr(pp.full_addr + 8u * cst, cphase);
     const T* tile = reinterpret_cast<const T*>(pp.stages + cst * Pipe<T, NI, STAGES>::STAGE_BYTES) + (8 * w) * SX + 8 * lane;
     uint32_t cs[8], r8[8];
     #pragma unroll
@@ -321,8 +320,8 @@ __device__ __forceinline__ void axis_loop(Pipe<T, NI, STAGES>& pp, int w, int la
       load_pair<T>(tile, t0, a, bb, p.offset, g.xok, g.zc);
       #pragma unroll
       for (int k = 0; k < 8; ++k) { zx[t0][k] += a[k]; zx[t1][k] += bb[k]; cs[k] += a[k] + bb[k]; }
-      r8[t0] = (a[0] + a[1] + a[2]) + (a[3] + a[4] + a[5]) + (a[6] + a[7]);
-      r8[t1] = (bb[0] + bb[1] + bb[2]) + (bb[3] + bb[4] + bb[5]) + (bb[6] + bb[7]);
+      r8[t0] = sum8(a);
+      r8[t1] = sum8(bb);
     }
     // YZ: warp reduce-scatter of the 8 plane sums; lane quad q ends with plane q's total
     const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
@@ -344,9 +343,9 @@ __device__ __forceinline__ void axis_loop(Pipe<T, NI, STAGES>& pp, int w, int la
     r1 += __shfl_xor_sync(0xffffffffu, r1, 2);
     r1 += __shfl_xor_sync(0xffffffffu, r1, 1);
     ptx::red_global_add_if(yz_col + y, r1, (lane & 3) == 0 && r1 != 0 && (lane >> 2) < g.zc);
-    add_owned<8>(pp.rows_addr + (uint32_t)(parity * RL::WORDS * 4) + 4 * (RL::XY + 8 * lane), cs);
+    add_owned<RL::SXY>(pp.rows_addr + (uint32_t)(parity * RL::WORDS * 4) + 4 * (RL::XY + lane), cs);
     __syncthreads();
-    pp.end_step(parity, col, y);
+    pp.end_step(parity, g.b, g.X0, g.Z0, y);
     parity ^= 1;
     if (++cst == STAGES) { cst = 0; cphase ^= 1u; }
     cur.advance(p);
@@ -369,7 +368,7 @@ __device__ __forceinline__ void oblique_loop(Pipe<T, NI, STAGES>& pp, int w, int
   while (!cur.done) {
     const int32_t y = cur.y();
     if (cur.c != col) { col = cur.c; g.set(p, col, w, lane); }
-    ptx::mbar_wait(&pp.full[cst], cphase);
+    ptx::mbar_wait_addr(pp.full_addr + 8u * cst, cphase);
     const T* tile = reinterpret_cast<const T*>(pp.stages + cst * Pipe<T, NI, STAGES>::STAGE_BYTES) + (8 * w) * SX + 8 * lane;
     uint32_t wd[16], wa[16], wp[24], wm[24];
     #pragma unroll
@@ -392,27 +391,27 @@ __device__ __forceinline__ void oblique_loop(Pipe<T, NI, STAGES>& pp, int w, int
     if (NI > DPM_IMG_X2M) merge_owned<22>(wm, lane);
     const uint32_t rp = pp.rows_addr + (uint32_t)(parity * RL::WORDS * 4);
     {
-      const uint32_t base = rp + 4 * (RL::DG + 8 * lane + 8 * w);
-      add_owned<8>(base, wd);
-      if (lane == 31) add_spill<7>(base, wd + 8, 0);
+      const uint32_t base = rp + 4 * (RL::DG + lane + w);
+      add_owned<RL::SOB>(base, wd);
+      if (lane == 31) add_spill<RL::SOB, 7>(base, wd + 8, 0);
     }
     if (NI > DPM_IMG_ANTI) {
-      const uint32_t base = rp + 4 * (RL::AN + 8 * lane - 8 * w + 56);
-      add_owned<8>(base, wa);
-      if (lane == 31) add_spill<7>(base, wa + 8, 0);
+      const uint32_t base = rp + 4 * (RL::AN + lane - w + 7);
+      add_owned<RL::SOB>(base, wa);
+      if (lane == 31) add_spill<RL::SOB, 7>(base, wa + 8, 0);
     }
     if (NI > DPM_IMG_X2P) {
-      const uint32_t base = rp + 4 * (RL::XP + 8 * lane + 16 * w);
-      add_owned<8>(base, wp);
-      if (lane >= 30) add_spill<14>(base, wp + 8, lane == 31 ? 0 : 8);
+      const uint32_t base = rp + 4 * (RL::XP + lane + 2 * w);
+      add_owned<RL::SOB>(base, wp);
+      if (lane >= 30) add_spill<RL::SOB, 14>(base, wp + 8, lane == 31 ? 0 : 8);
     }
     if (NI > DPM_IMG_X2M) {
-      const uint32_t base = rp + 4 * (RL::XM + 8 * lane - 16 * w + 112);
-      add_owned<8>(base, wm);
-      if (lane >= 30) add_spill<14>(base, wm + 8, lane == 31 ? 0 : 8);
+      const uint32_t base = rp + 4 * (RL::XM + lane - 2 * w + 14);
+      add_owned<RL::SOB>(base, wm);
+      if (lane >= 30) add_spill<RL::SOB, 14>(base, wm + 8, lane == 31 ? 0 : 8);
     }
     __syncthreads();
-    pp.end_step(parity, col, y);
+    pp.end_step(parity, g.b, g.X0, g.Z0, y);
     parity ^= 1;
     if (++cst == STAGES) { cst = 0; cphase ^= 1u; }
     cur.advance(p);
@@ -432,6 +431,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
   pp.rows = reinterpret_cast<uint32_t*>(smem + STAGES * P::STAGE_BYTES);
   pp.full = reinterpret_cast<uint64_t*>(pp.rows + 2 * RL::WORDS);
   pp.rows_addr = ptx::smem_addr(pp.rows);
+  pp.full_addr = ptx::smem_addr(pp.full);
   pp.tid = threadIdx.x;
   pp.pst = 0;
   const int lane = pp.tid & 31, warp = pp.tid >> 5;

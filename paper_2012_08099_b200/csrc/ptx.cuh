@@ -80,3 +80,17 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 }  // namespace ptx
 }  // namespace dpm
+
+namespace dpm {
+namespace ptx {
+__device__ __forceinline__ void mbar_wait_addr(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n"
+      "WAITA_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra WAITA_%=;\n\t}" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+}  // namespace ptx
+}  // namespace dpm
