@@ -6,23 +6,28 @@
 // Listing 1).
 //
 // Decomposition ("K1 project_stream"):
-//   column   = (volume b, x-tile of 256 voxels, z-tile of 64 planes)
-//   row-step = one y of one column: a 256 (x) x 64 (z) slice of plane-rows,
-//              fetched by ONE 4-D TMA box (x 256, y 1, z 64, b 1) into a
-//              shared-memory stage; a STAGES-deep mbarrier pipeline keeps
-//              several row-steps in flight per SM (zero-filled out of bounds).
-//   CTA      = 8 warps; warp w owns planes Z0+8w..+7, lane l owns x = X0+8l..+7,
-//              so each lane reduces an 8 (x) x 8 (z) patch per row-step.
+//   column   = (volume b, x-tile of 256 voxels, z-tile of SZ = 8*NW planes)
+//   row-step = one y of one column: a 256 (x) x SZ (z) slice of plane-rows,
+//              fetched by ONE 4-D TMA box (x 256, y 1, z SZ, b 1) into a
+//              shared-memory stage of a STAGES-deep mbarrier pipeline (zero
+//              fill out of bounds; L2 evict_first so the stream does not evict
+//              the image rows being reduced into).
+//   CTA      = NW warps, warp w owns planes Z0+8w..+7, lane l owns x = X0+8l..+7:
+//              each lane reduces an 8 (x) x 8 (z) patch per row-step.  NW is
+//              the largest warp count whose register budget fits the order:
+//              12 (3 warps/SMSP, <= 168 regs) for K <= 4, 8 (<= 255 regs) above.
 //   ZX (x,z)  sum over y: 64 registers per lane, persistent across the
-//             row-steps of a column, flushed with red.global on column change.
+//             row-steps of a column (adds on the FMA pipe), flushed with
+//             red.global when the CTA's run leaves the column.
 //   XY and the oblique images (x + t z, y), t = 1, -1, 2, -2: plane pairs are
-//             folded into 8 / 15 / 22-cell register windows with 3-input adds,
-//             window overlap with lane+1 (+2) goes over warp shuffles, and each
-//             lane adds its 8 owned cells into the CTA's shared-memory row with
-//             red.shared (8 warps = 8 z-blocks of the same row).  After the
-//             row-step barrier the row is flushed to global memory with one
-//             coalesced red.global per non-zero cell and re-zeroed
-//             (double-buffered rows, one __syncthreads per row-step).
+//             folded into 8 / 15 / 22-cell register windows with 3-input adds;
+//             window overlap with lane+1 (+2) moves by predicated shfl.up, and
+//             each lane red.shared's its 8 owned cells into the CTA row, stored
+//             transposed (cell i at (i%8)*S + i/8, S = 4 mod 32) so those
+//             reductions and the flush reads are bank-conflict free.  After one
+//             __syncthreads per row-step the row is flushed to global memory
+//             (coalesced predicated red.global of non-zero cells) and re-zeroed;
+//             rows are double-buffered.
 //   YZ (y,z)  per-plane lane sums, warp reduce-scatter, one red.global per (z,y).
 // Work split: row-steps are grouped into y-bands sized so a band's image rows
 // stay L2-resident; within a band the (column, y) sequence is cut into equal
@@ -31,23 +36,20 @@
 // reach 2^32) and associative integer atomics: bit-identical to the reference.
 #include <cudaTypedefs.h>
 #include <mutex>
+#include <cstdlib>
 #include "dpm_common.cuh"
 #include "ptx.cuh"
 
 namespace dpm {
 
 constexpr int SX = 256;                // x-tile (elements)
-constexpr int SZ = 64;                 // z-tile (planes)
-constexpr int W1 = SX + SZ - 1;        // DIAG/ANTI row footprint of a tile (319)
-constexpr int W2 = SX + 2 * SZ - 2;    // X2P/X2M row footprint (382)
-constexpr int W1P = 320, W2P = 384;    // padded
-constexpr int THREADS = 512;   // 16 warps: 8 axis warps + 8 oblique warps
 
 struct StreamParams {
   int64_t L, M, N, B;
   int32_t offset;
   int64_t ntx, ntz, ncol;      // tiles along x, z; columns = B * ntz * ntx
   int64_t band;                // rows per y-band
+  uint32_t one;                // == 1 at run time: keeps the ZX adds on the FMA pipe (IMAD)
   ImageSet s;
 };
 
@@ -98,28 +100,15 @@ __device__ __forceinline__ void fold_pair(uint32_t* win, const uint32_t* a, cons
   }
 }
 
-// Window cells [8, 16) belong to lane+1 and [16, 24) to lane+2: shuffle them up
-// and add into the receiver's owned cells [0, 8).  The sender keeps its copy in
-// spill[] (lanes 31/30 add theirs to the CTA row: it belongs to the next tile).
-template <int NW>
-__device__ __forceinline__ void merge_spill(uint32_t* win, uint32_t* spill, int lane) {
-  #pragma unroll
-  for (int c = 8; c < NW; ++c) {
-    const int dl = c >> 3;
-    const uint32_t in = __shfl_up_sync(0xffffffffu, win[c], dl);
-    spill[c - 8] = win[c];
-    win[c & 7] += (lane >= dl) ? in : 0u;
-  }
-}
 
+// Window cells [8, 16) belong to lane+1 and [16, 24) to lane+2: shuffle them
+// up and add into the receiver's owned cells [0, 8) (predicated on the source
+// lane existing).  Cells [8, NW) stay intact: lanes 31/30 add theirs (the next
+// x-tile's halo) to the CTA row separately.
 template <int NW>
-__device__ __forceinline__ void merge_owned(uint32_t* win, int lane) {
+__device__ __forceinline__ void merge_owned(uint32_t* win, int) {
   #pragma unroll
-  for (int c = 8; c < NW; ++c) {
-    const int dl = c >> 3;
-    const uint32_t in = __shfl_up_sync(0xffffffffu, win[c], dl);
-    win[c & 7] += (lane >= dl) ? in : 0u;
-  }
+  for (int c = 8; c < NW; ++c) win[c & 7] = ptx::add_from_lane_below(win[c & 7], win[c], c >> 3);
 }
 
 // owned cells 8g..8g+7 of a transposed region with stride S: word (c*S + g);
@@ -140,6 +129,14 @@ __device__ __forceinline__ void add_spill(uint32_t addr, const uint32_t* spill, 
     if (c >= first) ptx::red_shared_add_dyn(addr + 4 * ((c & 7) * S + 1 + (c >> 3)), spill[c]);
 }
 
+
+// 8-value sum as four 3-input adds
+__device__ __forceinline__ uint32_t sum8(const uint32_t* v) {
+  const uint32_t s0 = v[0] + v[1] + v[2];
+  const uint32_t s1 = s0 + v[3] + v[4];
+  const uint32_t s2 = s1 + v[5] + v[6];
+  return s2 + v[7];
+}
 // Per-CTA cursor over its row-steps: bands in order; inside a band the CTA's
 // contiguous run of the (column, y) sequence.  Advances incrementally (the
 // 64-bit divisions happen once per band, not per row-step).
@@ -165,93 +162,17 @@ struct Cursor {
   __device__ __forceinline__ int32_t y() const { return y0 + yoff; }
 };
 
-// CTA-row regions for one parity, in a TRANSPOSED layout: cell i of a region
-// lives at word (i % 8) * S + i / 8 with S = 4 (mod 32).  A lane's 8 owned
-// cells are 8i'..8i'+7 with i' = lane + const, so one red.shared instruction
-// (fixed i % 8) hits 32 consecutive words -> no bank conflicts; a warp reading
-// 32 consecutive cells for the flush hits banks 4(i%8) + i/8 -> distinct too.
-template <int NI> struct RowLayout {
-  static constexpr int SXY = 36, SOB = 68;          // >= groups (32 / 48), = 4 mod 32
+
+// Per-(NI, NW) geometry of the CTA rows (transposed layout, see header).
+template <int NI, int NW> struct Geo {
+  static constexpr int SZ = 8 * NW;                    // z-tile
+  static constexpr int W1 = SX + SZ - 1;               // DIAG/ANTI row footprint
+  static constexpr int W2 = SX + 2 * SZ - 2;           // X2P/X2M row footprint
+  static constexpr int SXY = 36, SOB = 68;             // >= groups, = 4 (mod 32)
+  static_assert((W2 + 7) / 8 + 2 <= SOB, "row stride too small");
   static constexpr int XY = 0, DG = 8 * SXY, AN = DG + 8 * SOB, XP = AN + 8 * SOB, XM = XP + 8 * SOB;
   static constexpr int WORDS = NI <= 4 ? DG + 8 * SOB : NI == 5 ? AN + 8 * SOB : NI == 6 ? XP + 8 * SOB : XM + 8 * SOB;
-  __device__ static constexpr int addr(int region_base, int stride, int cell) { return region_base + (cell & 7) * stride + (cell >> 3); }
-};
-
-// 8-value sum as four 3-input adds
-__device__ __forceinline__ uint32_t sum8(const uint32_t* v) {
-  const uint32_t s0 = v[0] + v[1] + v[2];
-  const uint32_t s1 = s0 + v[3] + v[4];
-  const uint32_t s2 = s1 + v[5] + v[6];
-  return s2 + v[7];
-}
-
-template <typename T>
-__device__ __forceinline__ void load_pair(const T* tile, int t0, uint32_t* a, uint32_t* bb, int32_t off, bool xok, int zc) {
-  using V = typename Vec<T>::type;
-  unpack8<T>(*reinterpret_cast<const V*>(tile + t0 * SX), a, off);
-  unpack8<T>(*reinterpret_cast<const V*>(tile + (t0 + 1) * SX), bb, off);
-  if (((T)-1) < (T)0) {  // signed input: zero-filled (out-of-bounds) voxels must stay 0 after the offset
-    const bool ok0 = xok && t0 < zc, ok1 = xok && t0 + 1 < zc;
-    #pragma unroll
-    for (int k = 0; k < 8; ++k) { a[k] = ok0 ? a[k] : 0u; bb[k] = ok1 ? bb[k] : 0u; }
-  }
-}
-
-// Per-CTA pipeline state: TMA stages (full barriers), double-buffered CTA rows.
-// One __syncthreads per row-step separates "add into rows[parity]" from
-// "flush rows[parity]" and frees the consumed stage for the producer.
-template <typename T, int NI, int STAGES>
-struct Pipe {
-  using RL = RowLayout<NI>;
-  static constexpr uint32_t STAGE_BYTES = SZ * SX * sizeof(T);
-  const StreamParams* p;
-  const CUtensorMap* tmap;
-  uint8_t* stages;
-  uint32_t* rows;
-  uint64_t* full;
-  uint32_t rows_addr, full_addr;
-  int tid;
-  Cursor prod;   // producer (thread 0)
-  int pst;
-
-  __device__ __forceinline__ void issue() {
-    const int32_t per = (int32_t)(p->ntz * p->ntx);
-    const int32_t b = prod.c / per, r = prod.c - b * per;
-    const int32_t zt = r / (int32_t)p->ntx;
-    ptx::mbar_arrive_expect_tx(&full[pst], STAGE_BYTES);
-    ptx::tma_load_4d(stages + pst * STAGE_BYTES, tmap, &full[pst], (r - zt * (int32_t)p->ntx) * SX, prod.y(), zt * SZ, b);
-    prod.advance(*p);
-    if (++pst == STAGES) pst = 0;
-  }
-
-  // after the row-step barrier: refill the consumed stage, flush the CTA rows (4 cells per thread-op)
-  __device__ __forceinline__ void end_step(int parity, int32_t b, int64_t X0, int64_t Z0, int32_t y) {
-    if (tid == 0 && !prod.done) issue();
-    uint32_t* rw = rows + parity * RL::WORDS;
-    const int64_t rowid = (int64_t)b * p->M + y;
-    auto flush_region = [&](int base, int stride, int ncell, uint32_t* grow, int64_t g0, int64_t W) {
-      for (int i = tid; i < ncell; i += THREADS) {
-        uint32_t* cellp = rw + base + (i & 7) * stride + (i >> 3);
-        const uint32_t v = *cellp;
-        *cellp = 0;
-        const int64_t gi = g0 + i;
-        ptx::red_global_add_if(grow + gi, v, v != 0 && gi >= 0 && gi < W);
-      }
-    };
-    flush_region(RL::XY, RL::SXY, SX, p->s.img[DPM_IMG_XY] + rowid * p->L, X0, p->L);
-    {
-      const int64_t W = p->s.W[DPM_IMG_DIAG];
-      flush_region(RL::DG, RL::SOB, W1, p->s.img[DPM_IMG_DIAG] + rowid * W, X0 + Z0, W);
-      if (NI > DPM_IMG_ANTI)
-        flush_region(RL::AN, RL::SOB, W1, p->s.img[DPM_IMG_ANTI] + rowid * W, X0 - Z0 - 63 + p->N - 1, W);
-    }
-    if (NI > DPM_IMG_X2P) {
-      const int64_t W = p->s.W[DPM_IMG_X2P];
-      flush_region(RL::XP, RL::SOB, W2, p->s.img[DPM_IMG_X2P] + rowid * W, X0 + 2 * Z0, W);
-      if (NI > DPM_IMG_X2M)
-        flush_region(RL::XM, RL::SOB, W2, p->s.img[DPM_IMG_X2M] + rowid * W, X0 - 2 * Z0 - 126 + 2 * (p->N - 1), W);
-    }
-  }
+  static constexpr int THREADS = 32 * NW;
 };
 
 struct ColGeom {
@@ -259,7 +180,7 @@ struct ColGeom {
   int32_t b;
   int zc;
   bool xok;
-  __device__ __forceinline__ void set(const StreamParams& p, int32_t col, int w, int lane) {
+  __device__ __forceinline__ void set(const StreamParams& p, int32_t col, int SZ, int w, int lane) {
     const int32_t per = (int32_t)(p.ntz * p.ntx);
     b = col / per;
     const int32_t r = col - b * per;
@@ -270,21 +191,83 @@ struct ColGeom {
   }
 };
 
-// Axis warps (0..7): ZX registers, XY column sums, YZ plane sums.
-template <typename T, int NI, int STAGES>
-__device__ __forceinline__ void axis_loop(Pipe<T, NI, STAGES>& pp, int w, int lane) {
-  using RL = RowLayout<NI>;
-  const StreamParams& p = *pp.p;
+// one transposed region of a CTA row buffer -> global image row; [lo, hi) is
+// the valid local range (precomputed per column)
+__device__ __forceinline__ void flush_region(uint32_t* rw, int base, int stride, int ncell, int tid, int nthreads,
+                                             uint32_t* g, int lo, int hi) {
+  for (int i = tid; i < ncell; i += nthreads) {
+    uint32_t* cellp = rw + base + (i & 7) * stride + (i >> 3);
+    const uint32_t v = *cellp;
+    *cellp = 0;
+    ptx::red_global_add_if(g + i, v, v != 0 && i >= lo && i < hi);
+  }
+}
+
+// per-column flush geometry of one region: global offset of local cell 0 and valid range
+struct RegionCol {
+  int64_t g0;
+  int lo, hi;
+  __device__ __forceinline__ void set(int64_t g0_, int ncell, int64_t W) {
+    g0 = g0_;
+    lo = (int)imax64(0, -g0_);
+    hi = (int)imin64(ncell, W - g0_);
+  }
+};
+
+template <typename T, int NI, int NW, int STAGES>
+__global__ void __launch_bounds__(32 * NW, 1)
+project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
+  using G = Geo<NI, NW>;
+  using V = typename Vec<T>::type;
+  constexpr int SZ = G::SZ, THREADS = G::THREADS;
+  constexpr uint32_t STAGE_BYTES = SX * SZ * sizeof(T);
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* stages = smem;
+  uint32_t* rows = reinterpret_cast<uint32_t*>(smem + STAGES * STAGE_BYTES);   // [2][G::WORDS]
+  uint64_t* full = reinterpret_cast<uint64_t*>(rows + 2 * G::WORDS);           // [STAGES]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t rows_addr = ptx::smem_addr(rows), full_addr = ptx::smem_addr(full);
+
+  for (int i = tid; i < 2 * G::WORDS; i += THREADS) rows[i] = 0;
+  if (tid == 0) {
+    ptx::prefetch_tmap(&tmap);
+    for (int i = 0; i < STAGES; ++i) ptx::mbar_init(&full[i], 1);
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+
+  // producer (thread 0): STAGES row-steps ahead; refills after each row-step barrier
+  Cursor prod;
+  int pst = 0;
+  uint64_t evict_first = 0;
+  auto issue = [&]() {
+    const int32_t per = (int32_t)(p.ntz * p.ntx);
+    const int32_t b = prod.c / per, r = prod.c - b * per;
+    const int32_t zt = r / (int32_t)p.ntx;
+    ptx::mbar_arrive_expect_tx(&full[pst], STAGE_BYTES);
+    ptx::tma_load_4d_hint(stages + pst * STAGE_BYTES, &tmap, &full[pst], (r - zt * (int32_t)p.ntx) * SX, prod.y(),
+                          zt * SZ, b, evict_first);
+    prod.advance(p);
+    if (++pst == STAGES) pst = 0;
+  };
+  if (tid == 0) {
+    evict_first = ptx::policy_evict_first();
+    prod.init(p);
+    for (int i = 0; i < STAGES && !prod.done; ++i) issue();
+  }
+
   Cursor cur;
   cur.init(p);
   uint32_t zx[8][8];
   int32_t col = -1;
   ColGeom g;
-  g.zc = 0; g.xok = false;
+  g.X0 = g.Z0 = 0; g.b = 0; g.zc = 0; g.xok = false;
   uint32_t* zx_col = nullptr;
   uint32_t* yz_col = nullptr;
+  RegionCol rc[5];
   int cst = 0, parity = 0;
   uint32_t cphase = 0;
+
   auto flush_zx = [&]() {
     if (col < 0) return;
     #pragma unroll
@@ -294,161 +277,139 @@ __device__ __forceinline__ void axis_loop(Pipe<T, NI, STAGES>& pp, int w, int la
         ptx::red_global_add_if(zx_col + k * p.N + t, zx[t][k], zx[t][k] != 0 && g.xok && t < g.zc);
     }
   };
+
   while (!cur.done) {
     const int32_t y = cur.y();
     if (cur.c != col) {
       flush_zx();
       col = cur.c;
-      g.set(p, col, w, lane);
+      g.set(p, col, SZ, w, lane);
       #pragma unroll
       for (int t = 0; t < 8; ++t) {
         #pragma unroll
         for (int k = 0; k < 8; ++k) zx[t][k] = 0;
       }
       zx_col = p.s.img[DPM_IMG_ZX] + (int64_t)g.b * p.L * p.N + (g.X0 + 8 * lane) * p.N + g.Z0 + 8 * w;
+      rc[0].set(g.X0, SX, p.L);
+      rc[1].set(g.X0 + g.Z0, G::W1, p.s.W[DPM_IMG_DIAG]);
+      if (NI > DPM_IMG_ANTI) rc[2].set(g.X0 - g.Z0 - (SZ - 1) + p.N - 1, G::W1, p.s.W[DPM_IMG_ANTI]);
+      if (NI > DPM_IMG_X2P) rc[3].set(g.X0 + 2 * g.Z0, G::W2, p.s.W[DPM_IMG_X2P]);
+      if (NI > DPM_IMG_X2M) rc[4].set(g.X0 - 2 * g.Z0 - 2 * (SZ - 1) + 2 * (p.N - 1), G::W2, p.s.W[DPM_IMG_X2M]);
       yz_col = p.s.img[DPM_IMG_YZ] + (int64_t)g.b * p.M * p.N + (g.Z0 + 8 * w + (lane >> 2)) * p.M;
     }
-    ptx::mbar_wait_addr(pp.full_addr + 8u * cst, cphase);
-    const T* tile = reinterpret_cast<const T*>(pp.stages + cst * Pipe<T, NI, STAGES>::STAGE_BYTES) + (8 * w) * SX + 8 * lane;
+    ptx::mbar_wait_addr(full_addr + 8u * cst, cphase);
+    const T* tile = reinterpret_cast<const T*>(stages + cst * STAGE_BYTES) + (8 * w) * SX + 8 * lane;
+
     uint32_t cs[8], r8[8];
+    uint32_t wd[16], wa[16], wp[24], wm[24];
     #pragma unroll
     for (int i = 0; i < 8; ++i) cs[i] = 0;
-    #pragma unroll
-    for (int tp = 0; tp < 4; ++tp) {
-      const int t0 = 2 * tp, t1 = t0 + 1;
-      uint32_t a[8], bb[8];
-      load_pair<T>(tile, t0, a, bb, p.offset, g.xok, g.zc);
-      #pragma unroll
-      for (int k = 0; k < 8; ++k) { zx[t0][k] += a[k]; zx[t1][k] += bb[k]; cs[k] += a[k] + bb[k]; }
-      r8[t0] = sum8(a);
-      r8[t1] = sum8(bb);
-    }
-    // YZ: warp reduce-scatter of the 8 plane sums; lane quad q ends with plane q's total
-    const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
-    uint32_t r4[4], r2[2], r1;
-    #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t send = h16 ? r8[j] : r8[j + 4], keep = h16 ? r8[j + 4] : r8[j];
-      r4[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-    #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const uint32_t send = h8 ? r4[j] : r4[j + 2], keep = h8 ? r4[j + 2] : r4[j];
-      r2[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-    {
-      const uint32_t send = h4 ? r2[0] : r2[1], keep = h4 ? r2[1] : r2[0];
-      r1 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    r1 += __shfl_xor_sync(0xffffffffu, r1, 2);
-    r1 += __shfl_xor_sync(0xffffffffu, r1, 1);
-    ptx::red_global_add_if(yz_col + y, r1, (lane & 3) == 0 && r1 != 0 && (lane >> 2) < g.zc);
-    add_owned<RL::SXY>(pp.rows_addr + (uint32_t)(parity * RL::WORDS * 4) + 4 * (RL::XY + lane), cs);
-    __syncthreads();
-    pp.end_step(parity, g.b, g.X0, g.Z0, y);
-    parity ^= 1;
-    if (++cst == STAGES) { cst = 0; cphase ^= 1u; }
-    cur.advance(p);
-  }
-  flush_zx();
-}
-
-// Oblique warps (8..15): DIAG / ANTI / X2P / X2M windows.
-template <typename T, int NI, int STAGES>
-__device__ __forceinline__ void oblique_loop(Pipe<T, NI, STAGES>& pp, int w, int lane) {
-  using RL = RowLayout<NI>;
-  const StreamParams& p = *pp.p;
-  Cursor cur;
-  cur.init(p);
-  int32_t col = -1;
-  ColGeom g;
-  g.zc = 0; g.xok = false;
-  int cst = 0, parity = 0;
-  uint32_t cphase = 0;
-  while (!cur.done) {
-    const int32_t y = cur.y();
-    if (cur.c != col) { col = cur.c; g.set(p, col, w, lane); }
-    ptx::mbar_wait_addr(pp.full_addr + 8u * cst, cphase);
-    const T* tile = reinterpret_cast<const T*>(pp.stages + cst * Pipe<T, NI, STAGES>::STAGE_BYTES) + (8 * w) * SX + 8 * lane;
-    uint32_t wd[16], wa[16], wp[24], wm[24];
     #pragma unroll
     for (int i = 0; i < 16; ++i) { wd[i] = 0; wa[i] = 0; }
     #pragma unroll
     for (int i = 0; i < 24; ++i) { wp[i] = 0; wm[i] = 0; }
     #pragma unroll
     for (int tp = 0; tp < 4; ++tp) {
-      const int t0 = 2 * tp;
+      const int t0 = 2 * tp, t1 = t0 + 1;
       uint32_t a[8], bb[8];
-      load_pair<T>(tile, t0, a, bb, p.offset, g.xok, g.zc);
+      unpack8<T>(*reinterpret_cast<const V*>(tile + t0 * SX), a, p.offset);
+      unpack8<T>(*reinterpret_cast<const V*>(tile + t1 * SX), bb, p.offset);
+      if (((T)-1) < (T)0) {  // signed input: zero-filled (out-of-bounds) voxels must stay 0 after the offset
+        const bool ok0 = g.xok && t0 < g.zc, ok1 = g.xok && t1 < g.zc;
+        #pragma unroll
+        for (int k = 0; k < 8; ++k) { a[k] = ok0 ? a[k] : 0u; bb[k] = ok1 ? bb[k] : 0u; }
+      }
+      #pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        zx[t0][k] = ptx::mad_u32(a[k], p.one, zx[t0][k]);
+        zx[t1][k] = ptx::mad_u32(bb[k], p.one, zx[t1][k]);
+        cs[k] += a[k] + bb[k];
+      }
+      r8[t0] = sum8(a);
+      r8[t1] = sum8(bb);
       fold_pair<15>(wd, a, bb, t0, t0 + 1);
       if (NI > DPM_IMG_ANTI) fold_pair<15>(wa, a, bb, 7 - t0, 6 - t0);
       if (NI > DPM_IMG_X2P) fold_pair<22>(wp, a, bb, 2 * t0, 2 * t0 + 2);
       if (NI > DPM_IMG_X2M) fold_pair<22>(wm, a, bb, 14 - 2 * t0, 12 - 2 * t0);
     }
+
+    // ---- YZ: warp reduce-scatter of the 8 plane sums -> lane quad q holds plane q
+    {
+      const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+      uint32_t r4[4], r2[2], r1;
+      #pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t send = h16 ? r8[j] : r8[j + 4], keep = h16 ? r8[j + 4] : r8[j];
+        r4[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      }
+      #pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const uint32_t send = h8 ? r4[j] : r4[j + 2], keep = h8 ? r4[j + 2] : r4[j];
+        r2[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      }
+      {
+        const uint32_t send = h4 ? r2[0] : r2[1], keep = h4 ? r2[1] : r2[0];
+        r1 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      }
+      r1 += __shfl_xor_sync(0xffffffffu, r1, 2);
+      r1 += __shfl_xor_sync(0xffffffffu, r1, 1);
+      ptx::red_global_add_if(yz_col + y, r1, (lane & 3) == 0 && r1 != 0 && (lane >> 2) < g.zc);
+    }
+
+    // ---- merge window overlaps, add owned cells into the CTA rows ------------
     merge_owned<15>(wd, lane);
     if (NI > DPM_IMG_ANTI) merge_owned<15>(wa, lane);
     if (NI > DPM_IMG_X2P) merge_owned<22>(wp, lane);
     if (NI > DPM_IMG_X2M) merge_owned<22>(wm, lane);
-    const uint32_t rp = pp.rows_addr + (uint32_t)(parity * RL::WORDS * 4);
     {
-      const uint32_t base = rp + 4 * (RL::DG + lane + w);
-      add_owned<RL::SOB>(base, wd);
-      if (lane == 31) add_spill<RL::SOB, 7>(base, wd + 8, 0);
+      const uint32_t rp = rows_addr + (uint32_t)(parity * G::WORDS * 4);
+      add_owned<G::SXY>(rp + 4 * (G::XY + lane), cs);
+      {
+        const uint32_t base = rp + 4 * (G::DG + lane + w);
+        add_owned<G::SOB>(base, wd);
+        if (lane == 31) add_spill<G::SOB, 7>(base, wd + 8, 0);
+      }
+      if (NI > DPM_IMG_ANTI) {
+        const uint32_t base = rp + 4 * (G::AN + lane - w + NW - 1);
+        add_owned<G::SOB>(base, wa);
+        if (lane == 31) add_spill<G::SOB, 7>(base, wa + 8, 0);
+      }
+      if (NI > DPM_IMG_X2P) {
+        const uint32_t base = rp + 4 * (G::XP + lane + 2 * w);
+        add_owned<G::SOB>(base, wp);
+        if (lane >= 30) add_spill<G::SOB, 14>(base, wp + 8, lane == 31 ? 0 : 8);
+      }
+      if (NI > DPM_IMG_X2M) {
+        const uint32_t base = rp + 4 * (G::XM + lane - 2 * w + 2 * NW - 2);
+        add_owned<G::SOB>(base, wm);
+        if (lane >= 30) add_spill<G::SOB, 14>(base, wm + 8, lane == 31 ? 0 : 8);
+      }
     }
-    if (NI > DPM_IMG_ANTI) {
-      const uint32_t base = rp + 4 * (RL::AN + lane - w + 7);
-      add_owned<RL::SOB>(base, wa);
-      if (lane == 31) add_spill<RL::SOB, 7>(base, wa + 8, 0);
-    }
-    if (NI > DPM_IMG_X2P) {
-      const uint32_t base = rp + 4 * (RL::XP + lane + 2 * w);
-      add_owned<RL::SOB>(base, wp);
-      if (lane >= 30) add_spill<RL::SOB, 14>(base, wp + 8, lane == 31 ? 0 : 8);
-    }
-    if (NI > DPM_IMG_X2M) {
-      const uint32_t base = rp + 4 * (RL::XM + lane - 2 * w + 14);
-      add_owned<RL::SOB>(base, wm);
-      if (lane >= 30) add_spill<RL::SOB, 14>(base, wm + 8, lane == 31 ? 0 : 8);
-    }
+
     __syncthreads();
-    pp.end_step(parity, g.b, g.X0, g.Z0, y);
+    if (tid == 0 && !prod.done) issue();   // every warp is done with stage `cst`
+
+    // ---- flush this row-step's CTA rows -------------------------------------
+    {
+      uint32_t* rw = rows + parity * G::WORDS;
+      const int64_t rowid = (int64_t)g.b * p.M + y;
+      flush_region(rw, G::XY, G::SXY, SX, tid, THREADS, p.s.img[DPM_IMG_XY] + rowid * p.L + rc[0].g0, rc[0].lo, rc[0].hi);
+      const int64_t Wd = p.s.W[DPM_IMG_DIAG];
+      flush_region(rw, G::DG, G::SOB, G::W1, tid, THREADS, p.s.img[DPM_IMG_DIAG] + rowid * Wd + rc[1].g0, rc[1].lo, rc[1].hi);
+      if (NI > DPM_IMG_ANTI)
+        flush_region(rw, G::AN, G::SOB, G::W1, tid, THREADS, p.s.img[DPM_IMG_ANTI] + rowid * Wd + rc[2].g0, rc[2].lo, rc[2].hi);
+      if (NI > DPM_IMG_X2P) {
+        const int64_t W2g = p.s.W[DPM_IMG_X2P];
+        flush_region(rw, G::XP, G::SOB, G::W2, tid, THREADS, p.s.img[DPM_IMG_X2P] + rowid * W2g + rc[3].g0, rc[3].lo, rc[3].hi);
+        if (NI > DPM_IMG_X2M)
+          flush_region(rw, G::XM, G::SOB, G::W2, tid, THREADS, p.s.img[DPM_IMG_X2M] + rowid * W2g + rc[4].g0, rc[4].lo, rc[4].hi);
+      }
+    }
     parity ^= 1;
     if (++cst == STAGES) { cst = 0; cphase ^= 1u; }
     cur.advance(p);
   }
-}
-
-template <typename T, int NI, int STAGES>
-__global__ void __launch_bounds__(THREADS, 1)
-project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
-  using RL = RowLayout<NI>;
-  using P = Pipe<T, NI, STAGES>;
-  extern __shared__ __align__(128) uint8_t smem[];
-  P pp;
-  pp.p = &p;
-  pp.tmap = &tmap;
-  pp.stages = smem;
-  pp.rows = reinterpret_cast<uint32_t*>(smem + STAGES * P::STAGE_BYTES);
-  pp.full = reinterpret_cast<uint64_t*>(pp.rows + 2 * RL::WORDS);
-  pp.rows_addr = ptx::smem_addr(pp.rows);
-  pp.full_addr = ptx::smem_addr(pp.full);
-  pp.tid = threadIdx.x;
-  pp.pst = 0;
-  const int lane = pp.tid & 31, warp = pp.tid >> 5;
-  for (int i = pp.tid; i < 2 * RL::WORDS; i += THREADS) pp.rows[i] = 0;
-  if (pp.tid == 0) {
-    ptx::prefetch_tmap(&tmap);
-    for (int i = 0; i < STAGES; ++i) ptx::mbar_init(&pp.full[i], 1);
-    ptx::fence_barrier_init();
-  }
-  __syncthreads();
-  if (pp.tid == 0) {
-    pp.prod.init(p);
-    for (int i = 0; i < STAGES && !pp.prod.done; ++i) pp.issue();
-  }
-  // warps 0..7: ZX / XY / YZ;  warps 8..15: obliques.  Warp w and w+8 read the same planes.
-  if (warp < 8) axis_loop<T, NI, STAGES>(pp, warp, lane);
-  else oblique_loop<T, NI, STAGES>(pp, warp - 8, lane);
+  flush_zx();
 }
 
 // ---------------------------------------------------------------------------
@@ -480,27 +441,53 @@ static bool stream_eligible(const dpm_volume_desc* d, const void* vox) {
 
 size_t project_stream_workspace(const dpm_volume_desc*, int) { return 0; }
 
-template <typename T> struct StageCount { static constexpr int value = sizeof(T) == 1 ? 8 : 5; };
+// warps per CTA by image count: as many as the per-lane register budget allows
+template <int NI> struct WarpsFor { static constexpr int value = NI <= 5 ? 12 : 8; };  // 3 warps/SMSP cap at 168 regs; 2 allow 255
+// stages: as many 4-D boxes as fit next to the row buffers (<= 227 KB)
+template <typename T, int NI> struct StagesFor {
+  static constexpr int NW = WarpsFor<NI>::value;
+  static constexpr int BOX = SX * 8 * NW * (int)sizeof(T);
+  static constexpr int ROWS = 2 * Geo<NI, NW>::WORDS * 4;
+  static constexpr int value = ((220 * 1024 - ROWS) / BOX) > 8 ? 8 : ((220 * 1024 - ROWS) / BOX);
+};
 
 template <typename T, int NI>
-static int launch_one(const CUtensorMap& map, int grid, cudaStream_t st, const StreamParams& p) {
-  constexpr int S = StageCount<T>::value;
-  constexpr size_t bytes = (size_t)S * SZ * SX * sizeof(T) + 2 * RowLayout<NI>::WORDS * 4 + S * 8;
+static int launch_one(const dpm_volume_desc* d, const void* vox, int grid, cudaStream_t st, StreamParams p) {
+  constexpr int NW = WarpsFor<NI>::value;
+  constexpr int S = StagesFor<T, NI>::value;
+  constexpr int SZ = 8 * NW;
+  constexpr size_t bytes = (size_t)S * SX * SZ * sizeof(T) + 2 * Geo<NI, NW>::WORDS * 4 + S * 8;
+  static_assert(bytes <= 227 * 1024, "shared memory budget");
+  const int64_t es = sizeof(T);
+  CUtensorMap map;
+  const cuuint64_t dims[4] = {(cuuint64_t)d->L, (cuuint64_t)d->M, (cuuint64_t)d->N, (cuuint64_t)d->B};
+  const cuuint64_t strides[3] = {(cuuint64_t)(d->stride_y * es), (cuuint64_t)(d->stride_z * es),
+                                 (cuuint64_t)((d->B > 1 ? d->stride_b : d->stride_z * d->N) * es)};
+  const cuuint32_t box[4] = {SX, 1, SZ, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = encode_fn()(&map, sizeof(T) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16,
+                                 4, const_cast<void*>(vox), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return -1;  // not describable by TMA: generic path
+  p.ntz = (d->N + SZ - 1) / SZ;
+  p.ncol = p.ntx * p.ntz * d->B;
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(project_stream_kernel<T, NI, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(project_stream_kernel<T, NI, NW, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   });
-  project_stream_kernel<T, NI, S><<<grid, THREADS, bytes, st>>>(map, p);
+  project_stream_kernel<T, NI, NW, S><<<(int)imin64(grid, p.ncol * d->M), 32 * NW, bytes, st>>>(map, p);
   return DPM_OK;
 }
 
 template <typename T>
-static int launch_typed(int n_img, const CUtensorMap& map, int grid, cudaStream_t st, const StreamParams& p) {
+static int launch_typed(int n_img, const dpm_volume_desc* d, const void* vox, int grid, cudaStream_t st,
+                        const StreamParams& p) {
   switch (n_img) {
-    case 4: return launch_one<T, 4>(map, grid, st, p);
-    case 5: return launch_one<T, 5>(map, grid, st, p);
-    case 6: return launch_one<T, 6>(map, grid, st, p);
-    default: return launch_one<T, 7>(map, grid, st, p);
+    case 4: return launch_one<T, 4>(d, vox, grid, st, p);
+    case 5: return launch_one<T, 5>(d, vox, grid, st, p);
+    case 6: return launch_one<T, 6>(d, vox, grid, st, p);
+    default: return launch_one<T, 7>(d, vox, grid, st, p);
   }
 }
 
@@ -508,22 +495,11 @@ int launch_project_stream(const dpm_volume_desc* d, const void* vox, const Image
                           cudaStream_t st, bool* handled) {
   *handled = false;
   if (s.n_img < 4 || !stream_eligible(d, vox)) return DPM_OK;
-  const int64_t es = d->dtype == DPM_U8 ? 1 : 2;
-  CUtensorMap map;
-  const cuuint64_t dims[4] = {(cuuint64_t)d->L, (cuuint64_t)d->M, (cuuint64_t)d->N, (cuuint64_t)d->B};
-  const cuuint64_t strides[3] = {(cuuint64_t)(d->stride_y * es), (cuuint64_t)(d->stride_z * es),
-                                 (cuuint64_t)((d->B > 1 ? d->stride_b : d->stride_z * d->N) * es)};
-  const cuuint32_t box[4] = {SX, 1, SZ, 1};
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
-  const CUresult r = encode_fn()(&map, d->dtype == DPM_U8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16,
-                                 4, const_cast<void*>(vox), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return DPM_OK;  // not describable by TMA: generic path
   StreamParams p;
   p.L = d->L; p.M = d->M; p.N = d->N; p.B = d->B; p.offset = d->offset;
-  p.ntx = (d->L + SX - 1) / SX; p.ntz = (d->N + SZ - 1) / SZ;
-  p.ncol = p.ntx * p.ntz * d->B;
+  p.ntx = (d->L + SX - 1) / SX;
+  p.ntz = 0; p.ncol = 0;  // set per warp count in launch_one
+  p.one = 1;
   p.s = s;
   // y-band: keep one band's image rows (plus the YZ cells) within ~40 MB of L2
   int64_t row_bytes = 0;
@@ -534,12 +510,13 @@ int launch_project_stream(const dpm_volume_desc* d, const void* vox, const Image
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = (int)imin64(sms, p.ncol * d->M);
+  int rc;
   switch (d->dtype) {
-    case DPM_U8: launch_typed<uint8_t>(s.n_img, map, grid, st, p); break;
-    case DPM_U16: launch_typed<uint16_t>(s.n_img, map, grid, st, p); break;
-    default: launch_typed<int16_t>(s.n_img, map, grid, st, p); break;
+    case DPM_U8: rc = launch_typed<uint8_t>(s.n_img, d, vox, sms, st, p); break;
+    case DPM_U16: rc = launch_typed<uint16_t>(s.n_img, d, vox, sms, st, p); break;
+    default: rc = launch_typed<int16_t>(s.n_img, d, vox, sms, st, p); break;
   }
+  if (rc < 0) return DPM_OK;   // TMA could not describe it: generic kernel
   note_launches(1);
   *handled = true;
   DPM_CUDA_CHECK_LAUNCH();
