@@ -39,6 +39,9 @@
 #include <cstdlib>
 #include "dpm_common.cuh"
 #include "ptx.cuh"
+#ifndef DPM_SKIP
+#define DPM_SKIP 0   // development bisection: 1 flush, 2 row atomics+merges, 4 YZ, 8 folds, 16 zx/cs/r8
+#endif
 
 namespace dpm {
 
@@ -319,6 +322,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
         #pragma unroll
         for (int k = 0; k < 8; ++k) { a[k] = ok0 ? a[k] : 0u; bb[k] = ok1 ? bb[k] : 0u; }
       }
+      if (!(DPM_SKIP & 16))
       #pragma unroll
       for (int k = 0; k < 8; ++k) {
         zx[t0][k] = ptx::mad_u32(a[k], p.one, zx[t0][k]);
@@ -327,14 +331,16 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
       }
       r8[t0] = sum8(a);
       r8[t1] = sum8(bb);
+      if (!(DPM_SKIP & 8)) {
       fold_pair<15>(wd, a, bb, t0, t0 + 1);
       if (NI > DPM_IMG_ANTI) fold_pair<15>(wa, a, bb, 7 - t0, 6 - t0);
       if (NI > DPM_IMG_X2P) fold_pair<22>(wp, a, bb, 2 * t0, 2 * t0 + 2);
       if (NI > DPM_IMG_X2M) fold_pair<22>(wm, a, bb, 14 - 2 * t0, 12 - 2 * t0);
+      }
     }
 
     // ---- YZ: warp reduce-scatter of the 8 plane sums -> lane quad q holds plane q
-    {
+    if (!(DPM_SKIP & 4)) {
       const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
       uint32_t r4[4], r2[2], r1;
       #pragma unroll
@@ -357,11 +363,11 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     }
 
     // ---- merge window overlaps, add owned cells into the CTA rows ------------
+    if (!(DPM_SKIP & 2)) {
     merge_owned<15>(wd, lane);
     if (NI > DPM_IMG_ANTI) merge_owned<15>(wa, lane);
     if (NI > DPM_IMG_X2P) merge_owned<22>(wp, lane);
     if (NI > DPM_IMG_X2M) merge_owned<22>(wm, lane);
-    {
       const uint32_t rp = rows_addr + (uint32_t)(parity * G::WORDS * 4);
       add_owned<G::SXY>(rp + 4 * (G::XY + lane), cs);
       {
@@ -390,7 +396,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     if (tid == 0 && !prod.done) issue();   // every warp is done with stage `cst`
 
     // ---- flush this row-step's CTA rows -------------------------------------
-    {
+    if (!(DPM_SKIP & 1)) {
       uint32_t* rw = rows + parity * G::WORDS;
       const int64_t rowid = (int64_t)g.b * p.M + y;
       flush_region(rw, G::XY, G::SXY, SX, tid, THREADS, p.s.img[DPM_IMG_XY] + rowid * p.L + rc[0].g0, rc[0].lo, rc[0].hi);
