@@ -6,24 +6,26 @@
 // Listing 1).
 //
 // Decomposition ("K1 project_stream"):
-//   column   = (volume b, x-tile of 256 voxels, z-tile of SZ = 8*NW planes)
-//   row-step = one y of one column: a 256 (x) x SZ (z) slice of plane-rows,
-//              fetched by ONE 4-D TMA box (x 256, y 1, z SZ, b 1) into a
+//   column   = (volume b, x-tile of SX = 32*VX voxels, z-tile of SZ = 8*NW planes)
+//   row-step = one y of one column: an SX (x) x SZ (z) slice of plane-rows,
+//              fetched by ONE 4-D TMA box (x SX, y 1, z SZ, b 1) into a
 //              shared-memory stage of a STAGES-deep mbarrier pipeline (zero
 //              fill out of bounds; L2 evict_first so the stream does not evict
 //              the image rows being reduced into).
-//   CTA      = NW warps, warp w owns planes Z0+8w..+7, lane l owns x = X0+8l..+7:
-//              each lane reduces an 8 (x) x 8 (z) patch per row-step.  NW is
+//   CTA      = NW warps, warp w owns planes Z0+8w..+7, lane l owns x = X0+VX*l..+VX-1:
+//              each lane reduces a VX (x) x 8 (z) patch per row-step (VX = 8, or
+//              4 for narrow volumes such as the 128^3 batch).  NW is
 //              the largest warp count whose register budget fits the order:
 //              12 (3 warps/SMSP, <= 168 regs) for K <= 4, 8 (<= 255 regs) above.
-//   ZX (x,z)  sum over y: 64 registers per lane, persistent across the
+//   ZX (x,z)  sum over y: 8*VX registers per lane, persistent across the
 //             row-steps of a column (adds on the FMA pipe), flushed with
 //             red.global when the CTA's run leaves the column.
 //   XY and the oblique images (x + t z, y), t = 1, -1, 2, -2: plane pairs are
-//             folded into 8 / 15 / 22-cell register windows with 3-input adds;
-//             window overlap with lane+1 (+2) moves by predicated shfl.up, and
-//             each lane red.shared's its 8 owned cells into the CTA row, stored
-//             transposed (cell i at (i%8)*S + i/8, S = 4 mod 32) so those
+//             folded into VX / VX+7 / VX+14-cell register windows with 3-input
+//             adds; window overlap with higher lanes moves by predicated
+//             shfl.up, and each lane red.shared's its VX owned cells into the
+//             CTA row, stored transposed (cell i at (i%VX)*S + i/VX,
+//             S = 32/VX mod 32) so those
 //             reductions and the flush reads are bank-conflict free.  After one
 //             __syncthreads per row-step the row is flushed to global memory
 //             (coalesced predicated red.global of non-zero cells) and re-zeroed;
@@ -45,8 +47,6 @@
 
 namespace dpm {
 
-constexpr int SX = 256;                // x-tile (elements)
-
 struct StreamParams {
   int64_t L, M, N, B;
   int32_t offset;
@@ -56,90 +56,98 @@ struct StreamParams {
   ImageSet s;
 };
 
-template <typename T> struct Vec;
-template <> struct Vec<uint16_t> { using type = uint4; };
-template <> struct Vec<int16_t>  { using type = uint4; };
-template <> struct Vec<uint8_t>  { using type = uint2; };
+// ---- VX-voxel lane vectors --------------------------------------------------
+template <typename T, int VX> struct Vec;
+template <> struct Vec<uint16_t, 8> { using type = uint4; };
+template <> struct Vec<int16_t, 8>  { using type = uint4; };
+template <> struct Vec<uint8_t, 8>  { using type = uint2; };
+template <> struct Vec<uint16_t, 4> { using type = uint2; };
+template <> struct Vec<int16_t, 4>  { using type = uint2; };
+template <> struct Vec<uint8_t, 4>  { using type = uint32_t; };
 
-template <typename T> __device__ __forceinline__ void unpack8(const typename Vec<T>::type& d, uint32_t* v, int32_t off);
-template <> __device__ __forceinline__ void unpack8<uint16_t>(const uint4& d, uint32_t* v, int32_t) {
-  const uint32_t w[4] = {d.x, d.y, d.z, d.w};
-  #pragma unroll
-  for (int i = 0; i < 4; ++i) { v[2 * i] = w[i] & 0xFFFFu; v[2 * i + 1] = w[i] >> 16; }
-}
-template <> __device__ __forceinline__ void unpack8<int16_t>(const uint4& d, uint32_t* v, int32_t off) {
-  const uint32_t w[4] = {d.x, d.y, d.z, d.w};
-  #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    v[2 * i] = (uint32_t)((int32_t)(int16_t)(w[i] & 0xFFFFu) + off);
-    v[2 * i + 1] = (uint32_t)((int32_t)(int16_t)(w[i] >> 16) + off);
-  }
-}
-template <> __device__ __forceinline__ void unpack8<uint8_t>(const uint2& d, uint32_t* v, int32_t) {
-  const uint32_t w[2] = {d.x, d.y};
-  #pragma unroll
-  for (int i = 0; i < 2; ++i) {
+template <typename T, int VX> struct Unpack;
+template <int VX> struct Unpack<uint16_t, VX> {
+  template <typename V> __device__ __forceinline__ static void run(const V& d, uint32_t* v, int32_t) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(&d);
     #pragma unroll
-    for (int j = 0; j < 4; ++j) v[4 * i + j] = (w[i] >> (8 * j)) & 0xFFu;
+    for (int i = 0; i < VX / 2; ++i) { v[2 * i] = w[i] & 0xFFFFu; v[2 * i + 1] = w[i] >> 16; }
   }
-}
+};
+template <int VX> struct Unpack<int16_t, VX> {
+  template <typename V> __device__ __forceinline__ static void run(const V& d, uint32_t* v, int32_t off) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(&d);
+    #pragma unroll
+    for (int i = 0; i < VX / 2; ++i) {
+      v[2 * i] = (uint32_t)((int32_t)(int16_t)(w[i] & 0xFFFFu) + off);
+      v[2 * i + 1] = (uint32_t)((int32_t)(int16_t)(w[i] >> 16) + off);
+    }
+  }
+};
+template <int VX> struct Unpack<uint8_t, VX> {
+  template <typename V> __device__ __forceinline__ static void run(const V& d, uint32_t* v, int32_t) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(&d);
+    #pragma unroll
+    for (int i = 0; i < VX / 4; ++i) {
+      #pragma unroll
+      for (int j = 0; j < 4; ++j) v[4 * i + j] = (w[i] >> (8 * j)) & 0xFFu;
+    }
+  }
+};
 
-// win[c] += a[c - OA] + b[c - OB] for every window cell the plane pair
-// (a = plane t, b = plane t+1) reaches.  Called with OA/OB that are constants
-// after unrolling, so every index is resolved at compile time (3-input adds).
+// win[c] += a[c - OA] + b[c - OB] over the cells the plane pair reaches (a =
+// plane t, b = plane t+1); OA/OB are constants after unrolling.
 //   DIAG c = k + t:        OA = t,        OB = t + 1
 //   ANTI c = k - t + 7:    OA = 7 - t,    OB = 6 - t
 //   X2P  c = k + 2t:       OA = 2t,       OB = 2t + 2
 //   X2M  c = k - 2t + 14:  OA = 14 - 2t,  OB = 12 - 2t
-template <int NW>
+template <int NW, int VX>
 __device__ __forceinline__ void fold_pair(uint32_t* win, const uint32_t* a, const uint32_t* b, int OA, int OB) {
   #pragma unroll
   for (int c = 0; c < NW; ++c) {
     const int ka = c - OA, kb = c - OB;
-    const bool ha = ka >= 0 && ka < 8, hb = kb >= 0 && kb < 8;
+    const bool ha = ka >= 0 && ka < VX, hb = kb >= 0 && kb < VX;
     if (ha && hb) win[c] += a[ka] + b[kb];
     else if (ha) win[c] += a[ka];
     else if (hb) win[c] += b[kb];
   }
 }
 
-
-// Window cells [8, 16) belong to lane+1 and [16, 24) to lane+2: shuffle them
-// up and add into the receiver's owned cells [0, 8) (predicated on the source
-// lane existing).  Cells [8, NW) stay intact: lanes 31/30 add theirs (the next
-// x-tile's halo) to the CTA row separately.
-template <int NW>
-__device__ __forceinline__ void merge_owned(uint32_t* win, int) {
+// Window cell c >= VX belongs to lane + c/VX (slot c % VX): shuffle up and add
+// (predicated on the source lane existing).  Cells [VX, NW) stay intact for the
+// halo reductions of the top lanes.
+template <int NW, int VX>
+__device__ __forceinline__ void merge_owned(uint32_t* win) {
   #pragma unroll
-  for (int c = 8; c < NW; ++c) win[c & 7] = ptx::add_from_lane_below(win[c & 7], win[c], c >> 3);
+  for (int c = VX; c < NW; ++c) win[c % VX] = ptx::add_from_lane_below(win[c % VX], win[c], c / VX);
 }
 
-// owned cells 8g..8g+7 of a transposed region with stride S: word (c*S + g);
+// owned cells VX*g .. VX*g+VX-1 of a transposed region with stride S: word c*S + g;
 // `addr` = region byte address + 4*g
-template <int S>
+template <int S, int VX>
 __device__ __forceinline__ void add_owned(uint32_t addr, const uint32_t* win) {
-  ptx::red_shared_add<0 * S * 4>(addr, win[0]); ptx::red_shared_add<1 * S * 4>(addr, win[1]);
-  ptx::red_shared_add<2 * S * 4>(addr, win[2]); ptx::red_shared_add<3 * S * 4>(addr, win[3]);
-  ptx::red_shared_add<4 * S * 4>(addr, win[4]); ptx::red_shared_add<5 * S * 4>(addr, win[5]);
-  ptx::red_shared_add<6 * S * 4>(addr, win[6]); ptx::red_shared_add<7 * S * 4>(addr, win[7]);
-}
-
-// window cells 8+c (c < NS) of group g = cells of group g + 1 + c/8, slot c % 8
-template <int S, int NS>
-__device__ __forceinline__ void add_spill(uint32_t addr, const uint32_t* spill, int first) {
   #pragma unroll
-  for (int c = 0; c < NS; ++c)
-    if (c >= first) ptx::red_shared_add_dyn(addr + 4 * ((c & 7) * S + 1 + (c >> 3)), spill[c]);
+  for (int c = 0; c < VX; ++c) ptx::red_shared_add_dyn(addr + 4 * c * S, win[c]);
 }
 
-
-// 8-value sum as four 3-input adds
-__device__ __forceinline__ uint32_t sum8(const uint32_t* v) {
-  const uint32_t s0 = v[0] + v[1] + v[2];
-  const uint32_t s1 = s0 + v[3] + v[4];
-  const uint32_t s2 = s1 + v[5] + v[6];
-  return s2 + v[7];
+// halo: window cells whose owner lane would be >= 32 (next x-tile) go straight into the CTA row
+template <int S, int VX, int NW>
+__device__ __forceinline__ void add_halo(uint32_t addr, const uint32_t* win, int lane) {
+  #pragma unroll
+  for (int c = VX; c < NW; ++c)
+    if (lane + c / VX >= 32) ptx::red_shared_add_dyn(addr + 4 * ((c % VX) * S + c / VX), win[c]);
 }
+
+// VX-value sums with 3-input adds
+template <int VX> __device__ __forceinline__ uint32_t sumv(const uint32_t* v) {
+  if (VX == 8) {
+    const uint32_t s0 = v[0] + v[1] + v[2];
+    const uint32_t s1 = s0 + v[3] + v[4];
+    const uint32_t s2 = s1 + v[5] + v[6];
+    return s2 + v[7];
+  }
+  return (v[0] + v[1] + v[2]) + v[VX - 1];
+}
+
 // Per-CTA cursor over its row-steps: bands in order; inside a band the CTA's
 // contiguous run of the (column, y) sequence.  Advances incrementally (the
 // 64-bit divisions happen once per band, not per row-step).
@@ -166,15 +174,20 @@ struct Cursor {
 };
 
 
-// Per-(NI, NW) geometry of the CTA rows (transposed layout, see header).
-template <int NI, int NW> struct Geo {
+// Per-(NI, NW, VX) geometry of the CTA rows (transposed layout, see header).
+__host__ __device__ constexpr int stride_for(int need, int VX) {
+  // smallest S >= need with S = 32/VX (mod 32)
+  return ((need - (32 / VX) + 31) / 32) * 32 + (32 / VX);
+}
+template <int NI, int NW, int VX> struct Geo {
+  static constexpr int SX = 32 * VX;                   // x-tile
   static constexpr int SZ = 8 * NW;                    // z-tile
   static constexpr int W1 = SX + SZ - 1;               // DIAG/ANTI row footprint
   static constexpr int W2 = SX + 2 * SZ - 2;           // X2P/X2M row footprint
-  static constexpr int SXY = 36, SOB = 68;             // >= groups, = 4 (mod 32)
-  static_assert((W2 + 7) / 8 + 2 <= SOB, "row stride too small");
-  static constexpr int XY = 0, DG = 8 * SXY, AN = DG + 8 * SOB, XP = AN + 8 * SOB, XM = XP + 8 * SOB;
-  static constexpr int WORDS = NI <= 4 ? DG + 8 * SOB : NI == 5 ? AN + 8 * SOB : NI == 6 ? XP + 8 * SOB : XM + 8 * SOB;
+  static constexpr int SXY = stride_for(32 + 1, VX);
+  static constexpr int SOB = stride_for((W2 + VX - 1) / VX + 2, VX);
+  static constexpr int XY = 0, DG = VX * SXY, AN = DG + VX * SOB, XP = AN + VX * SOB, XM = XP + VX * SOB;
+  static constexpr int WORDS = NI <= 4 ? DG + VX * SOB : NI == 5 ? AN + VX * SOB : NI == 6 ? XP + VX * SOB : XM + VX * SOB;
   static constexpr int THREADS = 32 * NW;
 };
 
@@ -183,23 +196,24 @@ struct ColGeom {
   int32_t b;
   int zc;
   bool xok;
-  __device__ __forceinline__ void set(const StreamParams& p, int32_t col, int SZ, int w, int lane) {
+  __device__ __forceinline__ void set(const StreamParams& p, int32_t col, int SX, int SZ, int VX, int w, int lane) {
     const int32_t per = (int32_t)(p.ntz * p.ntx);
     b = col / per;
     const int32_t r = col - b * per;
     Z0 = (int64_t)(r / (int32_t)p.ntx) * SZ;
     X0 = (int64_t)(r % (int32_t)p.ntx) * SX;
     zc = (int)imax64(0, imin64(8, p.N - (Z0 + 8 * w)));
-    xok = X0 + 8 * lane < p.L;
+    xok = X0 + VX * lane < p.L;
   }
 };
 
 // one transposed region of a CTA row buffer -> global image row; [lo, hi) is
 // the valid local range (precomputed per column)
+template <int VX>
 __device__ __forceinline__ void flush_region(uint32_t* rw, int base, int stride, int ncell, int tid, int nthreads,
                                              uint32_t* g, int lo, int hi) {
   for (int i = tid; i < ncell; i += nthreads) {
-    uint32_t* cellp = rw + base + (i & 7) * stride + (i >> 3);
+    uint32_t* cellp = rw + base + (i % VX) * stride + (i / VX);
     const uint32_t v = *cellp;
     *cellp = 0;
     ptx::red_global_add_if(g + i, v, v != 0 && i >= lo && i < hi);
@@ -217,12 +231,13 @@ struct RegionCol {
   }
 };
 
-template <typename T, int NI, int NW, int STAGES>
+template <typename T, int NI, int NW, int VX, int STAGES>
 __global__ void __launch_bounds__(32 * NW, 1)
 project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
-  using G = Geo<NI, NW>;
-  using V = typename Vec<T>::type;
-  constexpr int SZ = G::SZ, THREADS = G::THREADS;
+  using G = Geo<NI, NW, VX>;
+  using V = typename Vec<T, VX>::type;
+  constexpr int SX = G::SX, SZ = G::SZ, THREADS = G::THREADS;
+  constexpr int N1 = VX + 7, N2 = VX + 14;             // oblique window widths
   constexpr uint32_t STAGE_BYTES = SX * SZ * sizeof(T);
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stages = smem;
@@ -261,7 +276,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
 
   Cursor cur;
   cur.init(p);
-  uint32_t zx[8][8];
+  uint32_t zx[8][VX];
   int32_t col = -1;
   ColGeom g;
   g.X0 = g.Z0 = 0; g.b = 0; g.zc = 0; g.xok = false;
@@ -274,7 +289,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
   auto flush_zx = [&]() {
     if (col < 0) return;
     #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < VX; ++k) {
       #pragma unroll
       for (int t = 0; t < 8; ++t)
         ptx::red_global_add_if(zx_col + k * p.N + t, zx[t][k], zx[t][k] != 0 && g.xok && t < g.zc);
@@ -286,61 +301,58 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     if (cur.c != col) {
       flush_zx();
       col = cur.c;
-      g.set(p, col, SZ, w, lane);
+      g.set(p, col, SX, SZ, VX, w, lane);
       #pragma unroll
       for (int t = 0; t < 8; ++t) {
         #pragma unroll
-        for (int k = 0; k < 8; ++k) zx[t][k] = 0;
+        for (int k = 0; k < VX; ++k) zx[t][k] = 0;
       }
-      zx_col = p.s.img[DPM_IMG_ZX] + (int64_t)g.b * p.L * p.N + (g.X0 + 8 * lane) * p.N + g.Z0 + 8 * w;
+      zx_col = p.s.img[DPM_IMG_ZX] + (int64_t)g.b * p.L * p.N + (g.X0 + VX * lane) * p.N + g.Z0 + 8 * w;
+      yz_col = p.s.img[DPM_IMG_YZ] + (int64_t)g.b * p.M * p.N + (g.Z0 + 8 * w + (lane >> 2)) * p.M;
       rc[0].set(g.X0, SX, p.L);
       rc[1].set(g.X0 + g.Z0, G::W1, p.s.W[DPM_IMG_DIAG]);
       if (NI > DPM_IMG_ANTI) rc[2].set(g.X0 - g.Z0 - (SZ - 1) + p.N - 1, G::W1, p.s.W[DPM_IMG_ANTI]);
       if (NI > DPM_IMG_X2P) rc[3].set(g.X0 + 2 * g.Z0, G::W2, p.s.W[DPM_IMG_X2P]);
       if (NI > DPM_IMG_X2M) rc[4].set(g.X0 - 2 * g.Z0 - 2 * (SZ - 1) + 2 * (p.N - 1), G::W2, p.s.W[DPM_IMG_X2M]);
-      yz_col = p.s.img[DPM_IMG_YZ] + (int64_t)g.b * p.M * p.N + (g.Z0 + 8 * w + (lane >> 2)) * p.M;
     }
     ptx::mbar_wait_addr(full_addr + 8u * cst, cphase);
-    const T* tile = reinterpret_cast<const T*>(stages + cst * STAGE_BYTES) + (8 * w) * SX + 8 * lane;
+    const T* tile = reinterpret_cast<const T*>(stages + cst * STAGE_BYTES) + (8 * w) * SX + VX * lane;
 
-    uint32_t cs[8], r8[8];
-    uint32_t wd[16], wa[16], wp[24], wm[24];
+    uint32_t cs[VX], r8[8];
+    uint32_t wd[N1], wa[N1], wp[N2], wm[N2];
     #pragma unroll
-    for (int i = 0; i < 8; ++i) cs[i] = 0;
+    for (int i = 0; i < VX; ++i) cs[i] = 0;
     #pragma unroll
-    for (int i = 0; i < 16; ++i) { wd[i] = 0; wa[i] = 0; }
+    for (int i = 0; i < N1; ++i) { wd[i] = 0; wa[i] = 0; }
     #pragma unroll
-    for (int i = 0; i < 24; ++i) { wp[i] = 0; wm[i] = 0; }
+    for (int i = 0; i < N2; ++i) { wp[i] = 0; wm[i] = 0; }
     #pragma unroll
     for (int tp = 0; tp < 4; ++tp) {
       const int t0 = 2 * tp, t1 = t0 + 1;
-      uint32_t a[8], bb[8];
-      unpack8<T>(*reinterpret_cast<const V*>(tile + t0 * SX), a, p.offset);
-      unpack8<T>(*reinterpret_cast<const V*>(tile + t1 * SX), bb, p.offset);
+      uint32_t a[VX], bb[VX];
+      Unpack<T, VX>::run(*reinterpret_cast<const V*>(tile + t0 * SX), a, p.offset);
+      Unpack<T, VX>::run(*reinterpret_cast<const V*>(tile + t1 * SX), bb, p.offset);
       if (((T)-1) < (T)0) {  // signed input: zero-filled (out-of-bounds) voxels must stay 0 after the offset
         const bool ok0 = g.xok && t0 < g.zc, ok1 = g.xok && t1 < g.zc;
         #pragma unroll
-        for (int k = 0; k < 8; ++k) { a[k] = ok0 ? a[k] : 0u; bb[k] = ok1 ? bb[k] : 0u; }
+        for (int k = 0; k < VX; ++k) { a[k] = ok0 ? a[k] : 0u; bb[k] = ok1 ? bb[k] : 0u; }
       }
-      if (!(DPM_SKIP & 16))
       #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < VX; ++k) {
         zx[t0][k] = ptx::mad_u32(a[k], p.one, zx[t0][k]);
         zx[t1][k] = ptx::mad_u32(bb[k], p.one, zx[t1][k]);
         cs[k] += a[k] + bb[k];
       }
-      r8[t0] = sum8(a);
-      r8[t1] = sum8(bb);
-      if (!(DPM_SKIP & 8)) {
-      fold_pair<15>(wd, a, bb, t0, t0 + 1);
-      if (NI > DPM_IMG_ANTI) fold_pair<15>(wa, a, bb, 7 - t0, 6 - t0);
-      if (NI > DPM_IMG_X2P) fold_pair<22>(wp, a, bb, 2 * t0, 2 * t0 + 2);
-      if (NI > DPM_IMG_X2M) fold_pair<22>(wm, a, bb, 14 - 2 * t0, 12 - 2 * t0);
-      }
+      r8[t0] = sumv<VX>(a);
+      r8[t1] = sumv<VX>(bb);
+      fold_pair<N1, VX>(wd, a, bb, t0, t0 + 1);
+      if (NI > DPM_IMG_ANTI) fold_pair<N1, VX>(wa, a, bb, 7 - t0, 6 - t0);
+      if (NI > DPM_IMG_X2P) fold_pair<N2, VX>(wp, a, bb, 2 * t0, 2 * t0 + 2);
+      if (NI > DPM_IMG_X2M) fold_pair<N2, VX>(wm, a, bb, 14 - 2 * t0, 12 - 2 * t0);
     }
 
     // ---- YZ: warp reduce-scatter of the 8 plane sums -> lane quad q holds plane q
-    if (!(DPM_SKIP & 4)) {
+    {
       const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
       uint32_t r4[4], r2[2], r1;
       #pragma unroll
@@ -362,33 +374,33 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
       ptx::red_global_add_if(yz_col + y, r1, (lane & 3) == 0 && r1 != 0 && (lane >> 2) < g.zc);
     }
 
-    // ---- merge window overlaps, add owned cells into the CTA rows ------------
-    if (!(DPM_SKIP & 2)) {
-    merge_owned<15>(wd, lane);
-    if (NI > DPM_IMG_ANTI) merge_owned<15>(wa, lane);
-    if (NI > DPM_IMG_X2P) merge_owned<22>(wp, lane);
-    if (NI > DPM_IMG_X2M) merge_owned<22>(wm, lane);
+    // ---- merge window overlaps, add owned cells (and the tile's halo) into the CTA rows
+    merge_owned<N1, VX>(wd);
+    if (NI > DPM_IMG_ANTI) merge_owned<N1, VX>(wa);
+    if (NI > DPM_IMG_X2P) merge_owned<N2, VX>(wp);
+    if (NI > DPM_IMG_X2M) merge_owned<N2, VX>(wm);
+    {
       const uint32_t rp = rows_addr + (uint32_t)(parity * G::WORDS * 4);
-      add_owned<G::SXY>(rp + 4 * (G::XY + lane), cs);
+      add_owned<G::SXY, VX>(rp + 4 * (G::XY + lane), cs);
       {
-        const uint32_t base = rp + 4 * (G::DG + lane + w);
-        add_owned<G::SOB>(base, wd);
-        if (lane == 31) add_spill<G::SOB, 7>(base, wd + 8, 0);
+        const uint32_t base = rp + 4 * (G::DG + lane + (8 / VX) * w);
+        add_owned<G::SOB, VX>(base, wd);
+        add_halo<G::SOB, VX, N1>(base, wd, lane);
       }
       if (NI > DPM_IMG_ANTI) {
-        const uint32_t base = rp + 4 * (G::AN + lane - w + NW - 1);
-        add_owned<G::SOB>(base, wa);
-        if (lane == 31) add_spill<G::SOB, 7>(base, wa + 8, 0);
+        const uint32_t base = rp + 4 * (G::AN + lane + (8 / VX) * (NW - 1 - w));
+        add_owned<G::SOB, VX>(base, wa);
+        add_halo<G::SOB, VX, N1>(base, wa, lane);
       }
       if (NI > DPM_IMG_X2P) {
-        const uint32_t base = rp + 4 * (G::XP + lane + 2 * w);
-        add_owned<G::SOB>(base, wp);
-        if (lane >= 30) add_spill<G::SOB, 14>(base, wp + 8, lane == 31 ? 0 : 8);
+        const uint32_t base = rp + 4 * (G::XP + lane + (16 / VX) * w);
+        add_owned<G::SOB, VX>(base, wp);
+        add_halo<G::SOB, VX, N2>(base, wp, lane);
       }
       if (NI > DPM_IMG_X2M) {
-        const uint32_t base = rp + 4 * (G::XM + lane - 2 * w + 2 * NW - 2);
-        add_owned<G::SOB>(base, wm);
-        if (lane >= 30) add_spill<G::SOB, 14>(base, wm + 8, lane == 31 ? 0 : 8);
+        const uint32_t base = rp + 4 * (G::XM + lane + (16 / VX) * (NW - 1 - w));
+        add_owned<G::SOB, VX>(base, wm);
+        add_halo<G::SOB, VX, N2>(base, wm, lane);
       }
     }
 
@@ -396,19 +408,19 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     if (tid == 0 && !prod.done) issue();   // every warp is done with stage `cst`
 
     // ---- flush this row-step's CTA rows -------------------------------------
-    if (!(DPM_SKIP & 1)) {
+    {
       uint32_t* rw = rows + parity * G::WORDS;
       const int64_t rowid = (int64_t)g.b * p.M + y;
-      flush_region(rw, G::XY, G::SXY, SX, tid, THREADS, p.s.img[DPM_IMG_XY] + rowid * p.L + rc[0].g0, rc[0].lo, rc[0].hi);
+      flush_region<VX>(rw, G::XY, G::SXY, SX, tid, THREADS, p.s.img[DPM_IMG_XY] + rowid * p.L + rc[0].g0, rc[0].lo, rc[0].hi);
       const int64_t Wd = p.s.W[DPM_IMG_DIAG];
-      flush_region(rw, G::DG, G::SOB, G::W1, tid, THREADS, p.s.img[DPM_IMG_DIAG] + rowid * Wd + rc[1].g0, rc[1].lo, rc[1].hi);
+      flush_region<VX>(rw, G::DG, G::SOB, G::W1, tid, THREADS, p.s.img[DPM_IMG_DIAG] + rowid * Wd + rc[1].g0, rc[1].lo, rc[1].hi);
       if (NI > DPM_IMG_ANTI)
-        flush_region(rw, G::AN, G::SOB, G::W1, tid, THREADS, p.s.img[DPM_IMG_ANTI] + rowid * Wd + rc[2].g0, rc[2].lo, rc[2].hi);
+        flush_region<VX>(rw, G::AN, G::SOB, G::W1, tid, THREADS, p.s.img[DPM_IMG_ANTI] + rowid * Wd + rc[2].g0, rc[2].lo, rc[2].hi);
       if (NI > DPM_IMG_X2P) {
         const int64_t W2g = p.s.W[DPM_IMG_X2P];
-        flush_region(rw, G::XP, G::SOB, G::W2, tid, THREADS, p.s.img[DPM_IMG_X2P] + rowid * W2g + rc[3].g0, rc[3].lo, rc[3].hi);
+        flush_region<VX>(rw, G::XP, G::SOB, G::W2, tid, THREADS, p.s.img[DPM_IMG_X2P] + rowid * W2g + rc[3].g0, rc[3].lo, rc[3].hi);
         if (NI > DPM_IMG_X2M)
-          flush_region(rw, G::XM, G::SOB, G::W2, tid, THREADS, p.s.img[DPM_IMG_X2M] + rowid * W2g + rc[4].g0, rc[4].lo, rc[4].hi);
+          flush_region<VX>(rw, G::XM, G::SOB, G::W2, tid, THREADS, p.s.img[DPM_IMG_X2M] + rowid * W2g + rc[4].g0, rc[4].lo, rc[4].hi);
       }
     }
     parity ^= 1;
@@ -434,12 +446,14 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+static int lane_width(const dpm_volume_desc* d) { return d->L > 128 ? 8 : 4; }
+
 static bool stream_eligible(const dpm_volume_desc* d, const void* vox) {
   const int64_t es = d->dtype == DPM_U8 ? 1 : 2;
-  if (d->L < 64 || d->N < 8) return false;
+  if (d->L < 32 || d->N < 8) return false;
   if ((d->stride_y * es) % 16 || (d->stride_z * es) % 16) return false;
   if (d->B > 1 && (d->stride_b * es) % 16) return false;
-  if (d->L % 8) return false;  // a lane vector never straddles the row end
+  if (d->L % lane_width(d)) return false;  // a lane vector never straddles the row end
   if (reinterpret_cast<uintptr_t>(vox) % 16) return false;
   if (d->L > 0x7fffffffLL || d->M > 0x7fffffffLL || d->N > 0x7fffffffLL || d->B > 0x7fffffffLL) return false;
   return encode_fn() != nullptr;
@@ -447,54 +461,63 @@ static bool stream_eligible(const dpm_volume_desc* d, const void* vox) {
 
 size_t project_stream_workspace(const dpm_volume_desc*, int) { return 0; }
 
-// warps per CTA by image count: as many as the per-lane register budget allows
-template <int NI> struct WarpsFor { static constexpr int value = NI <= 5 ? 12 : 8; };  // 3 warps/SMSP cap at 168 regs; 2 allow 255
-// stages: as many 4-D boxes as fit next to the row buffers (<= 227 KB)
-template <typename T, int NI> struct StagesFor {
-  static constexpr int NW = WarpsFor<NI>::value;
-  static constexpr int BOX = SX * 8 * NW * (int)sizeof(T);
-  static constexpr int ROWS = 2 * Geo<NI, NW>::WORDS * 4;
-  static constexpr int value = ((220 * 1024 - ROWS) / BOX) > 8 ? 8 : ((220 * 1024 - ROWS) / BOX);
+// warps per CTA: 12 (3 warps/SMSP, <= 168 registers) unless the 8-wide lanes
+// of orders >= 5 need more registers (then 8 warps, <= 255 registers); the
+// 4-wide lanes of order 3 fit 128 registers, so 16 warps (128-plane z-tiles)
+template <int NI, int VX> struct WarpsFor { static constexpr int value = (VX == 8 && NI >= 6) ? 8 : (VX == 4 && NI == 4) ? 16 : 12; };
+// stages: as many 4-D boxes as fit next to the row buffers
+template <typename T, int NI, int VX> struct StagesFor {
+  static constexpr int NW = WarpsFor<NI, VX>::value;
+  static constexpr int BOX = 32 * VX * 8 * NW * (int)sizeof(T);
+  static constexpr int ROWS = 2 * Geo<NI, NW, VX>::WORDS * 4;
+  static constexpr int FIT = (220 * 1024 - ROWS) / BOX;
+  static constexpr int value = FIT > 12 ? 12 : FIT;
 };
 
-template <typename T, int NI>
+template <typename T, int NI, int VX>
 static int launch_one(const dpm_volume_desc* d, const void* vox, int grid, cudaStream_t st, StreamParams p) {
-  constexpr int NW = WarpsFor<NI>::value;
-  constexpr int S = StagesFor<T, NI>::value;
-  constexpr int SZ = 8 * NW;
-  constexpr size_t bytes = (size_t)S * SX * SZ * sizeof(T) + 2 * Geo<NI, NW>::WORDS * 4 + S * 8;
+  constexpr int NW = WarpsFor<NI, VX>::value;
+  constexpr int S = StagesFor<T, NI, VX>::value;
+  using G = Geo<NI, NW, VX>;
+  constexpr size_t bytes = (size_t)S * G::SX * G::SZ * sizeof(T) + 2 * G::WORDS * 4 + S * 8;
   static_assert(bytes <= 227 * 1024, "shared memory budget");
   const int64_t es = sizeof(T);
   CUtensorMap map;
   const cuuint64_t dims[4] = {(cuuint64_t)d->L, (cuuint64_t)d->M, (cuuint64_t)d->N, (cuuint64_t)d->B};
   const cuuint64_t strides[3] = {(cuuint64_t)(d->stride_y * es), (cuuint64_t)(d->stride_z * es),
                                  (cuuint64_t)((d->B > 1 ? d->stride_b : d->stride_z * d->N) * es)};
-  const cuuint32_t box[4] = {SX, 1, SZ, 1};
+  const cuuint32_t box[4] = {(cuuint32_t)G::SX, 1, (cuuint32_t)G::SZ, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   const CUresult r = encode_fn()(&map, sizeof(T) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16,
                                  4, const_cast<void*>(vox), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return -1;  // not describable by TMA: generic path
-  p.ntz = (d->N + SZ - 1) / SZ;
+  p.ntx = (d->L + G::SX - 1) / G::SX;
+  p.ntz = (d->N + G::SZ - 1) / G::SZ;
   p.ncol = p.ntx * p.ntz * d->B;
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(project_stream_kernel<T, NI, NW, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(project_stream_kernel<T, NI, NW, VX, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   });
-  project_stream_kernel<T, NI, NW, S><<<(int)imin64(grid, p.ncol * d->M), 32 * NW, bytes, st>>>(map, p);
+  project_stream_kernel<T, NI, NW, VX, S><<<(int)imin64(grid, p.ncol * d->M), 32 * NW, bytes, st>>>(map, p);
   return DPM_OK;
 }
 
-template <typename T>
+template <typename T, int VX>
 static int launch_typed(int n_img, const dpm_volume_desc* d, const void* vox, int grid, cudaStream_t st,
                         const StreamParams& p) {
   switch (n_img) {
-    case 4: return launch_one<T, 4>(d, vox, grid, st, p);
-    case 5: return launch_one<T, 5>(d, vox, grid, st, p);
-    case 6: return launch_one<T, 6>(d, vox, grid, st, p);
-    default: return launch_one<T, 7>(d, vox, grid, st, p);
+    case 4: return launch_one<T, 4, VX>(d, vox, grid, st, p);
+    case 5: return launch_one<T, 5, VX>(d, vox, grid, st, p);
+    case 6: return launch_one<T, 6, VX>(d, vox, grid, st, p);
+    default: return launch_one<T, 7, VX>(d, vox, grid, st, p);
   }
+}
+
+template <typename T>
+static int launch_vx(int n_img, const dpm_volume_desc* d, const void* vox, int grid, cudaStream_t st, const StreamParams& p) {
+  return lane_width(d) == 8 ? launch_typed<T, 8>(n_img, d, vox, grid, st, p) : launch_typed<T, 4>(n_img, d, vox, grid, st, p);
 }
 
 int launch_project_stream(const dpm_volume_desc* d, const void* vox, const ImageSet& s, void*, size_t,
@@ -503,8 +526,7 @@ int launch_project_stream(const dpm_volume_desc* d, const void* vox, const Image
   if (s.n_img < 4 || !stream_eligible(d, vox)) return DPM_OK;
   StreamParams p;
   p.L = d->L; p.M = d->M; p.N = d->N; p.B = d->B; p.offset = d->offset;
-  p.ntx = (d->L + SX - 1) / SX;
-  p.ntz = 0; p.ncol = 0;  // set per warp count in launch_one
+  p.ntx = p.ntz = p.ncol = 0;  // set per lane width / warp count in launch_one
   p.one = 1;
   p.s = s;
   // y-band: keep one band's image rows (plus the YZ cells) within ~40 MB of L2
@@ -518,9 +540,9 @@ int launch_project_stream(const dpm_volume_desc* d, const void* vox, const Image
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int rc;
   switch (d->dtype) {
-    case DPM_U8: rc = launch_typed<uint8_t>(s.n_img, d, vox, sms, st, p); break;
-    case DPM_U16: rc = launch_typed<uint16_t>(s.n_img, d, vox, sms, st, p); break;
-    default: rc = launch_typed<int16_t>(s.n_img, d, vox, sms, st, p); break;
+    case DPM_U8: rc = launch_vx<uint8_t>(s.n_img, d, vox, sms, st, p); break;
+    case DPM_U16: rc = launch_vx<uint16_t>(s.n_img, d, vox, sms, st, p); break;
+    default: rc = launch_vx<int16_t>(s.n_img, d, vox, sms, st, p); break;
   }
   if (rc < 0) return DPM_OK;   // TMA could not describe it: generic kernel
   note_launches(1);

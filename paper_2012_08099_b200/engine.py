@@ -238,3 +238,26 @@ def ints_to_limbs(values) -> np.ndarray:
         for k in range(4):
             out[idx + (k,)] = (u >> (32 * k)) & 0xFFFFFFFF
     return out.view(np.int64)
+
+
+class GraphedMoments:
+    """The whole device pipeline for a fixed input tensor, captured once in a
+    CUDA graph and replayed (no per-call host work: ctypes calls, tensor-map
+    encoding and launches happen at capture time only)."""
+
+    def __init__(self, vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0, n_global: int | None = None):
+        self.vox = vox
+        self.order = order
+        self.stream = torch.cuda.Stream(device=vox.device)
+        self.stream.wait_stream(torch.cuda.current_stream(vox.device))
+        with torch.cuda.stream(self.stream):
+            self.out = moments(vox, order, offset=offset, z0=z0, n_global=n_global)   # warm-up, allocates
+            self.launches = self.out.launches
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, stream=self.stream):
+                moments(vox, order, offset=offset, z0=z0, n_global=n_global, out=self.out)
+        torch.cuda.current_stream(vox.device).wait_stream(self.stream)
+
+    def replay(self) -> DeviceMoments:
+        self.graph.replay()
+        return self.out

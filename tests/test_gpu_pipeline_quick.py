@@ -12,7 +12,8 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("dims,bits,order", [((5, 4, 3), 8, 3), ((7, 6, 5), 16, 4), ((9, 7, 5), 8, 6),
                                                ((64, 64, 64), 8, 3), ((33, 17, 20), 16, 6),
-                                               ((264, 19, 72), 16, 6), ((320, 9, 70), 8, 5)])
+                                               ((264, 19, 72), 16, 6), ((320, 9, 70), 8, 5),
+                                               ((128, 9, 100), 8, 6), ((100, 6, 99), 16, 5), ((64, 5, 97), 8, 4)])
 def test_dpm_matches_oracle(cuda, dims, bits, order):
     v = vm.random(dims, bits, seed=3)
     got = vm.dpm_moments(v, order)
@@ -21,7 +22,8 @@ def test_dpm_matches_oracle(cuda, dims, bits, order):
 
 
 @pytest.mark.parametrize("dims", [(1, 1, 1), (5, 3, 2), (16, 16, 16), (70, 9, 33), (64, 8, 8),
-                                  (256, 3, 64), (264, 5, 65), (512, 2, 130)])
+                                  (256, 3, 64), (264, 5, 65), (512, 2, 130), (128, 7, 130), (100, 5, 37),
+                                  (36, 4, 9), (132, 3, 100)])
 @pytest.mark.parametrize("bits", [8, 16])
 def test_projections_match_oracle(cuda, dims, bits):
     v = vm.random(dims, bits, seed=1)

@@ -30,19 +30,26 @@ def main():
              ("1024^3 u16 K6", (1024, 1024, 1024), torch.uint16, 6),
              ("1024^3 u16 K4", (1024, 1024, 1024), torch.uint16, 4),
              ("1024^3 u8 K3", (1024, 1024, 1024), torch.uint8, 3),
-             ("cfg5 2048^3 u16 K6", (2048, 2048, 2048), torch.uint16, 6)]
+             ("cfg5 2048^3 u16 K6", (2048, 2048, 2048), torch.uint16, 6),
+             ("cfg4 1024x128^3 u8 K3", (1024, 128, 128, 128), torch.uint8, 3)]
     for name, shape, dt, K in cases:
         if only and only not in name:
             continue
-        n = shape[0] * shape[1] * shape[2]
-        if dt == torch.uint16:
+        n = 1
+        for d in shape:
+            n *= d
+        if len(shape) == 4:
+            v = (torch.rand(shape, device="cuda") < 0.3).to(torch.uint8)
+        elif dt == torch.uint16:
             v = engine.synth_noise(shape[2], shape[1], 0, shape[0], 5)
         else:
             v = torch.randint(0, 256, shape, dtype=torch.uint8, device="cuda")
         nbytes = v.numel() * v.element_size()
         tp = timeit(lambda: engine.project(v, engine.num_images(K)))
+        imgs = engine.project(v, engine.num_images(K))
+        t2 = timeit(lambda: engine.moments2d_images(v, imgs, K))
         tm = timeit(lambda: engine.moments(v, K))
-        print(f"{name}: project {tp:.3f} ms ({nbytes / tp / 1e6:.0f} GB/s)  full {tm:.3f} ms "
+        print(f"{name}: project {tp:.3f} ms ({nbytes / tp / 1e6:.0f} GB/s)  moments2d {t2:.3f} ms  full {tm:.3f} ms "
               f"({nbytes / tm / 1e6:.0f} GB/s, {n / tm / 1e6:.0f} GVox/s)", flush=True)
         del v
         torch.cuda.empty_cache()
