@@ -41,6 +41,9 @@
 #include <cstdlib>
 #include "dpm_common.cuh"
 #include "ptx.cuh"
+#ifndef DPM_UNPACK_FMA
+#define DPM_UNPACK_FMA 0
+#endif
 #ifndef DPM_SKIP
 #define DPM_SKIP 0   // development bisection: 1 flush, 2 row atomics+merges, 4 YZ, 8 folds, 16 zx/cs/r8
 #endif
@@ -67,14 +70,25 @@ template <> struct Vec<uint8_t, 4>  { using type = uint32_t; };
 
 template <typename T, int VX> struct Unpack;
 template <int VX> struct Unpack<uint16_t, VX> {
-  template <typename V> __device__ __forceinline__ static void run(const V& d, uint32_t* v, int32_t) {
+  template <typename V> __device__ __forceinline__ static void run(const V& d, uint32_t* v, int32_t, uint32_t k16) {
     const uint32_t* w = reinterpret_cast<const uint32_t*>(&d);
+#if DPM_UNPACK_FMA
+    // k16 == 65536 at run time: IMAD.HI / IMAD keep the unpack on the FMA pipe
+    #pragma unroll
+    for (int i = 0; i < VX / 2; ++i) {
+      const uint32_t hi = ptx::mulhi_u32(w[i], k16);
+      v[2 * i + 1] = hi;
+      v[2 * i] = ptx::mad_u32(hi, 0u - k16, w[i]);
+    }
+#else
+    (void)k16;
     #pragma unroll
     for (int i = 0; i < VX / 2; ++i) { v[2 * i] = w[i] & 0xFFFFu; v[2 * i + 1] = w[i] >> 16; }
+#endif
   }
 };
 template <int VX> struct Unpack<int16_t, VX> {
-  template <typename V> __device__ __forceinline__ static void run(const V& d, uint32_t* v, int32_t off) {
+  template <typename V> __device__ __forceinline__ static void run(const V& d, uint32_t* v, int32_t off, uint32_t) {
     const uint32_t* w = reinterpret_cast<const uint32_t*>(&d);
     #pragma unroll
     for (int i = 0; i < VX / 2; ++i) {
@@ -84,7 +98,7 @@ template <int VX> struct Unpack<int16_t, VX> {
   }
 };
 template <int VX> struct Unpack<uint8_t, VX> {
-  template <typename V> __device__ __forceinline__ static void run(const V& d, uint32_t* v, int32_t) {
+  template <typename V> __device__ __forceinline__ static void run(const V& d, uint32_t* v, int32_t, uint32_t) {
     const uint32_t* w = reinterpret_cast<const uint32_t*>(&d);
     #pragma unroll
     for (int i = 0; i < VX / 4; ++i) {
@@ -238,6 +252,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
   using V = typename Vec<T, VX>::type;
   constexpr int SX = G::SX, SZ = G::SZ, THREADS = G::THREADS;
   constexpr int N1 = VX + 7, N2 = VX + 14;             // oblique window widths
+  constexpr bool TWO_PASS = NI >= 6 && VX == 8 && NW > 8;   // +-2z images in a second pass over the stage
   constexpr uint32_t STAGE_BYTES = SX * SZ * sizeof(T);
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stages = smem;
@@ -330,8 +345,8 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     for (int tp = 0; tp < 4; ++tp) {
       const int t0 = 2 * tp, t1 = t0 + 1;
       uint32_t a[VX], bb[VX];
-      Unpack<T, VX>::run(*reinterpret_cast<const V*>(tile + t0 * SX), a, p.offset);
-      Unpack<T, VX>::run(*reinterpret_cast<const V*>(tile + t1 * SX), bb, p.offset);
+      Unpack<T, VX>::run(*reinterpret_cast<const V*>(tile + t0 * SX), a, p.offset, p.one << 16);
+      Unpack<T, VX>::run(*reinterpret_cast<const V*>(tile + t1 * SX), bb, p.offset, p.one << 16);
       if (((T)-1) < (T)0) {  // signed input: zero-filled (out-of-bounds) voxels must stay 0 after the offset
         const bool ok0 = g.xok && t0 < g.zc, ok1 = g.xok && t1 < g.zc;
         #pragma unroll
@@ -347,8 +362,8 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
       r8[t1] = sumv<VX>(bb);
       fold_pair<N1, VX>(wd, a, bb, t0, t0 + 1);
       if (NI > DPM_IMG_ANTI) fold_pair<N1, VX>(wa, a, bb, 7 - t0, 6 - t0);
-      if (NI > DPM_IMG_X2P) fold_pair<N2, VX>(wp, a, bb, 2 * t0, 2 * t0 + 2);
-      if (NI > DPM_IMG_X2M) fold_pair<N2, VX>(wm, a, bb, 14 - 2 * t0, 12 - 2 * t0);
+      if (!TWO_PASS && NI > DPM_IMG_X2P) fold_pair<N2, VX>(wp, a, bb, 2 * t0, 2 * t0 + 2);
+      if (!TWO_PASS && NI > DPM_IMG_X2M) fold_pair<N2, VX>(wm, a, bb, 14 - 2 * t0, 12 - 2 * t0);
     }
 
     // ---- YZ: warp reduce-scatter of the 8 plane sums -> lane quad q holds plane q
@@ -377,8 +392,8 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     // ---- merge window overlaps, add owned cells (and the tile's halo) into the CTA rows
     merge_owned<N1, VX>(wd);
     if (NI > DPM_IMG_ANTI) merge_owned<N1, VX>(wa);
-    if (NI > DPM_IMG_X2P) merge_owned<N2, VX>(wp);
-    if (NI > DPM_IMG_X2M) merge_owned<N2, VX>(wm);
+    if (!TWO_PASS && NI > DPM_IMG_X2P) merge_owned<N2, VX>(wp);
+    if (!TWO_PASS && NI > DPM_IMG_X2M) merge_owned<N2, VX>(wm);
     {
       const uint32_t rp = rows_addr + (uint32_t)(parity * G::WORDS * 4);
       add_owned<G::SXY, VX>(rp + 4 * (G::XY + lane), cs);
@@ -391,6 +406,28 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
         const uint32_t base = rp + 4 * (G::AN + lane + (8 / VX) * (NW - 1 - w));
         add_owned<G::SOB, VX>(base, wa);
         add_halo<G::SOB, VX, N1>(base, wa, lane);
+      }
+      if (TWO_PASS) {
+        // second pass over the same stage for the (x +- 2z, y) images: keeps the
+        // live register set of order 6 within the 12-warp budget
+        #pragma unroll
+        for (int i = 0; i < N2; ++i) { wp[i] = 0; wm[i] = 0; }
+        #pragma unroll
+        for (int tp = 0; tp < 4; ++tp) {
+          const int t0 = 2 * tp, t1 = t0 + 1;
+          uint32_t a[VX], bb[VX];
+          Unpack<T, VX>::run(*reinterpret_cast<const V*>(tile + t0 * SX), a, p.offset, p.one << 16);
+          Unpack<T, VX>::run(*reinterpret_cast<const V*>(tile + t1 * SX), bb, p.offset, p.one << 16);
+          if (((T)-1) < (T)0) {
+            const bool ok0 = g.xok && t0 < g.zc, ok1 = g.xok && t1 < g.zc;
+            #pragma unroll
+            for (int k = 0; k < VX; ++k) { a[k] = ok0 ? a[k] : 0u; bb[k] = ok1 ? bb[k] : 0u; }
+          }
+          fold_pair<N2, VX>(wp, a, bb, 2 * t0, 2 * t0 + 2);
+          fold_pair<N2, VX>(wm, a, bb, 14 - 2 * t0, 12 - 2 * t0);
+        }
+        merge_owned<N2, VX>(wp);
+        merge_owned<N2, VX>(wm);
       }
       if (NI > DPM_IMG_X2P) {
         const uint32_t base = rp + 4 * (G::XP + lane + (16 / VX) * w);
@@ -464,7 +501,13 @@ size_t project_stream_workspace(const dpm_volume_desc*, int) { return 0; }
 // warps per CTA: 12 (3 warps/SMSP, <= 168 registers) unless the 8-wide lanes
 // of orders >= 5 need more registers (then 8 warps, <= 255 registers); the
 // 4-wide lanes of order 3 fit 128 registers, so 16 warps (128-plane z-tiles)
-template <int NI, int VX> struct WarpsFor { static constexpr int value = (VX == 8 && NI >= 6) ? 8 : (VX == 4 && NI == 4) ? 16 : 12; };
+template <int NI, int VX> struct WarpsFor {
+#ifdef DPM_K6_WARPS
+  static constexpr int value = (VX == 8 && NI >= 6) ? DPM_K6_WARPS : (VX == 4 && NI == 4) ? 16 : 12;
+#else
+  static constexpr int value = (VX == 4 && NI == 4) ? 16 : 12;
+#endif
+};
 // stages: as many 4-D boxes as fit next to the row buffers
 template <typename T, int NI, int VX> struct StagesFor {
   static constexpr int NW = WarpsFor<NI, VX>::value;

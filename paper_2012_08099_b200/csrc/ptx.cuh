@@ -148,3 +148,13 @@ __device__ __forceinline__ void tma_load_4d_hint(void* dst, const CUtensorMap* m
 }
 }  // namespace ptx
 }  // namespace dpm
+
+namespace dpm {
+namespace ptx {
+__device__ __forceinline__ uint32_t mulhi_u32(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+}  // namespace ptx
+}  // namespace dpm
