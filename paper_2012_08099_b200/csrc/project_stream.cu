@@ -38,7 +38,6 @@
 // reach 2^32) and associative integer atomics: bit-identical to the reference.
 #include <cudaTypedefs.h>
 #include <mutex>
-#include <cstdlib>
 #include "dpm_common.cuh"
 #include "ptx.cuh"
 #ifndef DPM_NO_ZX
@@ -133,13 +132,15 @@ __device__ __forceinline__ void fold_pair(uint32_t* win, const uint32_t* a, cons
 // (predicated on the source lane existing).  Cells [VX, NW) stay intact for the
 // halo reductions of the top lanes.
 template <int NW, int VX>
-__device__ __forceinline__ void merge_owned(uint32_t* win) {
-  // all shuffles first, then the adds: the shuffle latencies overlap
+__device__ __forceinline__ void merge_owned(uint32_t* win, const uint32_t* mk) {
+  // all shuffles first, then the adds: the shuffle latencies overlap.  shfl.up
+  // hands lanes below the shift their own value; mk[d] = (lane >= d) zeroes it
+  // inside one IMAD (FMA pipe) instead of a select plus an add.
   uint32_t in[NW];
   #pragma unroll
-  for (int c = VX; c < NW; ++c) in[c] = ptx::from_lane_below(win[c], c / VX);
+  for (int c = VX; c < NW; ++c) in[c] = __shfl_up_sync(0xffffffffu, win[c], c / VX);
   #pragma unroll
-  for (int c = VX; c < NW; ++c) win[c % VX] += in[c];
+  for (int c = VX; c < NW; ++c) win[c % VX] = ptx::mad_u32(in[c], mk[c / VX], win[c % VX]);
 }
 
 // owned cells VX*g .. VX*g+VX-1 of a transposed region with stride S: word c*S + g;
@@ -206,7 +207,7 @@ template <int NI, int NW, int VX> struct Geo {
   static constexpr int W1 = SX + SZ - 1;               // DIAG/ANTI row footprint
   static constexpr int W2 = SX + 2 * SZ - 2;           // X2P/X2M row footprint
   static constexpr int SXY = stride_for(32 + 1, VX);
-  static constexpr int SOB = stride_for((W2 + VX - 1) / VX + 2, VX);
+  static constexpr int SOB = stride_for(((W2 + VX - 1) / VX + 3) / 4 * 4 + 2, VX);
   static constexpr int XY = 0, DG = VX * SXY, AN = DG + VX * SOB, XP = AN + VX * SOB, XM = XP + VX * SOB;
   static constexpr int WORDS = NI <= 4 ? DG + VX * SOB : NI == 5 ? AN + VX * SOB : NI == 6 ? XP + VX * SOB : XM + VX * SOB;
   static constexpr int THREADS = 32 * NW;
@@ -228,27 +229,52 @@ struct ColGeom {
   }
 };
 
-// one transposed region of a CTA row buffer -> global image row; [lo, hi) is
-// the valid local range (precomputed per column)
-template <int VX>
-__device__ __forceinline__ void flush_region(uint32_t* rw, int base, int stride, int ncell, int tid, int nthreads,
-                                             uint32_t* g, int lo, int hi) {
-  for (int i = tid; i < ncell; i += nthreads) {
-    uint32_t* cellp = rw + base + (i % VX) * stride + (i / VX);
-    const uint32_t v = *cellp;
-    *cellp = 0;
-    ptx::red_global_add_if(g + i, v, v != 0 && i >= lo && i < hi);
+// one transposed region of a CTA row buffer -> global image row.  Cell c sits
+// at word (c % VX) * S + c / VX, so one 16-byte word group of residue row r
+// holds cells VX*q + r + {0, VX, 2VX, 3VX}: one LDS.128 / STS.128 and four
+// immediate-offset reds per 4 cells.  `g` points at local cell 0 of the
+// global row; [lo, hi) is the part of the padded extent inside the row.
+// Cells past NCELL are never written (zero), so reducing them is harmless.
+template <int VX, int S, int NCELL, int THREADS>
+__device__ __forceinline__ void flush_region(uint32_t* rw, int tid, uint32_t* g, int lo, int hi) {
+  constexpr int WORDS = (NCELL + VX - 1) / VX;
+  constexpr int QCH = (WORDS + 3) / 4;
+  constexpr int NCH = VX * QCH;
+  static_assert(4 * QCH <= S, "row stride must cover the padded word groups");
+  const bool interior = lo == 0 && hi >= 4 * QCH * VX;    // uniform per CTA
+  #pragma unroll
+  for (int it = 0; it < (NCH + THREADS - 1) / THREADS; ++it) {
+    const int j = tid + it * THREADS;
+    if ((NCH % THREADS) != 0 && j >= NCH) break;
+    const int r = j % VX, q = 4 * (j / VX);
+    uint4* wp = reinterpret_cast<uint4*>(rw + r * S + q);
+    const uint4 v = *wp;
+    *wp = make_uint4(0u, 0u, 0u, 0u);
+    const int c0 = VX * q + r;
+    uint32_t* gp = g + c0;
+    if (interior) {
+      ptx::red_global_add_off<0>(gp, v.x);
+      ptx::red_global_add_off<4 * VX>(gp, v.y);
+      ptx::red_global_add_off<8 * VX>(gp, v.z);
+      ptx::red_global_add_off<12 * VX>(gp, v.w);
+    } else {
+      ptx::red_global_add_if(gp, v.x, c0 >= lo && c0 < hi);
+      ptx::red_global_add_if(gp + VX, v.y, c0 + VX >= lo && c0 + VX < hi);
+      ptx::red_global_add_if(gp + 2 * VX, v.z, c0 + 2 * VX >= lo && c0 + 2 * VX < hi);
+      ptx::red_global_add_if(gp + 3 * VX, v.w, c0 + 3 * VX >= lo && c0 + 3 * VX < hi);
+    }
   }
 }
 
-// per-column flush geometry of one region: global offset of local cell 0 and valid range
+// per-column flush geometry of one region: global offset of local cell 0 and
+// the local range [lo, hi) that lies inside the image row
 struct RegionCol {
   int64_t g0;
   int lo, hi;
-  __device__ __forceinline__ void set(int64_t g0_, int ncell, int64_t W) {
+  __device__ __forceinline__ void set(int64_t g0_, int64_t W) {
     g0 = g0_;
     lo = (int)imax64(0, -g0_);
-    hi = (int)imin64(ncell, W - g0_);
+    hi = (int)imin64(1 << 30, W - g0_);
   }
 };
 
@@ -296,6 +322,9 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     for (int i = 0; i < STAGES && !prod.done; ++i) issue();
   }
 
+  uint32_t mk[N2 / VX + 1];   // mk[d] = 1 where lane d below exists (window merges)
+  #pragma unroll
+  for (int d = 0; d <= N2 / VX; ++d) mk[d] = lane >= d ? p.one : 0u;
   Cursor cur;
   cur.init(p);
   uint32_t zx[8][VX];
@@ -331,11 +360,11 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
       }
       zx_col = p.s.img[DPM_IMG_ZX] + (int64_t)g.b * p.L * p.N + (g.X0 + VX * lane) * p.N + g.Z0 + 8 * w;
       yz_col = p.s.img[DPM_IMG_YZ] + (int64_t)g.b * p.M * p.N + (g.Z0 + 8 * w + (lane >> 2)) * p.M;
-      rc[0].set(g.X0, SX, p.L);
-      rc[1].set(g.X0 + g.Z0, G::W1, p.s.W[DPM_IMG_DIAG]);
-      if (NI > DPM_IMG_ANTI) rc[2].set(g.X0 - g.Z0 - (SZ - 1) + p.N - 1, G::W1, p.s.W[DPM_IMG_ANTI]);
-      if (NI > DPM_IMG_X2P) rc[3].set(g.X0 + 2 * g.Z0, G::W2, p.s.W[DPM_IMG_X2P]);
-      if (NI > DPM_IMG_X2M) rc[4].set(g.X0 - 2 * g.Z0 - 2 * (SZ - 1) + 2 * (p.N - 1), G::W2, p.s.W[DPM_IMG_X2M]);
+      rc[0].set(g.X0, p.L);
+      rc[1].set(g.X0 + g.Z0, p.s.W[DPM_IMG_DIAG]);
+      if (NI > DPM_IMG_ANTI) rc[2].set(g.X0 - g.Z0 - (SZ - 1) + p.N - 1, p.s.W[DPM_IMG_ANTI]);
+      if (NI > DPM_IMG_X2P) rc[3].set(g.X0 + 2 * g.Z0, p.s.W[DPM_IMG_X2P]);
+      if (NI > DPM_IMG_X2M) rc[4].set(g.X0 - 2 * g.Z0 - 2 * (SZ - 1) + 2 * (p.N - 1), p.s.W[DPM_IMG_X2M]);
     }
     ptx::mbar_wait_addr(full_addr + 8u * cst, cphase);
     const T* tile = reinterpret_cast<const T*>(stages + cst * STAGE_BYTES) + (8 * w) * SX + VX * lane;
@@ -402,10 +431,10 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     }
 
     // ---- merge window overlaps, add owned cells (and the tile's halo) into the CTA rows
-    merge_owned<N1, VX>(wd);
-    if (NI > DPM_IMG_ANTI) merge_owned<N1, VX>(wa);
-    if (!TWO_PASS && NI > DPM_IMG_X2P) merge_owned<N2, VX>(wp);
-    if (!TWO_PASS && NI > DPM_IMG_X2M) merge_owned<N2, VX>(wm);
+    merge_owned<N1, VX>(wd, mk);
+    if (NI > DPM_IMG_ANTI) merge_owned<N1, VX>(wa, mk);
+    if (!TWO_PASS && NI > DPM_IMG_X2P) merge_owned<N2, VX>(wp, mk);
+    if (!TWO_PASS && NI > DPM_IMG_X2M) merge_owned<N2, VX>(wm, mk);
     {
       const uint32_t rp = rows_addr + (uint32_t)(parity * G::WORDS * 4);
       add_owned<G::SXY, VX>(rp + 4 * (G::XY + lane), cs);
@@ -438,8 +467,8 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
           fold_pair<N2, VX>(wp, a, bb, 2 * t0, 2 * t0 + 2);
           fold_pair<N2, VX>(wm, a, bb, 14 - 2 * t0, 12 - 2 * t0);
         }
-        merge_owned<N2, VX>(wp);
-        merge_owned<N2, VX>(wm);
+        merge_owned<N2, VX>(wp, mk);
+        merge_owned<N2, VX>(wm, mk);
       }
       if (NI > DPM_IMG_X2P) {
         const uint32_t base = rp + 4 * (G::XP + lane + (16 / VX) * w);
@@ -460,16 +489,16 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     {
       uint32_t* rw = rows + parity * G::WORDS;
       const int64_t rowid = (int64_t)g.b * p.M + y;
-      flush_region<VX>(rw, G::XY, G::SXY, SX, tid, THREADS, p.s.img[DPM_IMG_XY] + rowid * p.L + rc[0].g0, rc[0].lo, rc[0].hi);
+      flush_region<VX, G::SXY, SX, THREADS>(rw + G::XY, tid, p.s.img[DPM_IMG_XY] + rowid * p.L + rc[0].g0, rc[0].lo, rc[0].hi);
       const int64_t Wd = p.s.W[DPM_IMG_DIAG];
-      flush_region<VX>(rw, G::DG, G::SOB, G::W1, tid, THREADS, p.s.img[DPM_IMG_DIAG] + rowid * Wd + rc[1].g0, rc[1].lo, rc[1].hi);
+      flush_region<VX, G::SOB, G::W1, THREADS>(rw + G::DG, tid, p.s.img[DPM_IMG_DIAG] + rowid * Wd + rc[1].g0, rc[1].lo, rc[1].hi);
       if (NI > DPM_IMG_ANTI)
-        flush_region<VX>(rw, G::AN, G::SOB, G::W1, tid, THREADS, p.s.img[DPM_IMG_ANTI] + rowid * Wd + rc[2].g0, rc[2].lo, rc[2].hi);
+        flush_region<VX, G::SOB, G::W1, THREADS>(rw + G::AN, tid, p.s.img[DPM_IMG_ANTI] + rowid * Wd + rc[2].g0, rc[2].lo, rc[2].hi);
       if (NI > DPM_IMG_X2P) {
         const int64_t W2g = p.s.W[DPM_IMG_X2P];
-        flush_region<VX>(rw, G::XP, G::SOB, G::W2, tid, THREADS, p.s.img[DPM_IMG_X2P] + rowid * W2g + rc[3].g0, rc[3].lo, rc[3].hi);
+        flush_region<VX, G::SOB, G::W2, THREADS>(rw + G::XP, tid, p.s.img[DPM_IMG_X2P] + rowid * W2g + rc[3].g0, rc[3].lo, rc[3].hi);
         if (NI > DPM_IMG_X2M)
-          flush_region<VX>(rw, G::XM, G::SOB, G::W2, tid, THREADS, p.s.img[DPM_IMG_X2M] + rowid * W2g + rc[4].g0, rc[4].lo, rc[4].hi);
+          flush_region<VX, G::SOB, G::W2, THREADS>(rw + G::XM, tid, p.s.img[DPM_IMG_X2M] + rowid * W2g + rc[4].g0, rc[4].lo, rc[4].hi);
       }
     }
     parity ^= 1;

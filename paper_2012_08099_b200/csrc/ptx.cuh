@@ -218,3 +218,13 @@ __host__ __device__ __forceinline__ uint64_t umma_desc(uint32_t smem_addr, uint3
 }
 }  // namespace ptx
 }  // namespace dpm
+
+namespace dpm {
+namespace ptx {
+// red.global.add.u32 [gptr + OFF] (unconditional; OFF in bytes)
+template <int OFF>
+__device__ __forceinline__ void red_global_add_off(uint32_t* gptr, uint32_t v) {
+  asm volatile("red.global.add.u32 [%0+%1], %2;" ::"l"(gptr), "n"(OFF), "r"(v) : "memory");
+}
+}  // namespace ptx
+}  // namespace dpm
