@@ -126,9 +126,23 @@ def project(vox: torch.Tensor, n_img: int, offset: int = 0, z0: int = 0,
     return imgs
 
 
+def workspace_bytes(vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0) -> int:
+    """Device scratch bytes ``moments`` needs for this volume and order."""
+    desc = make_desc(vox, offset, z0)
+    wsb = int(nat.lib().dpm_workspace_bytes(ctypes.byref(desc), order))
+    if wsb == 0:
+        raise ValueError("invalid volume descriptor")
+    return wsb
+
+
 def moments(vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0, n_global: int | None = None,
-            stream: torch.cuda.Stream | None = None, out: DeviceMoments | None = None) -> DeviceMoments:
-    """Whole pipeline (project -> exact 2D moments -> device epilogue)."""
+            stream: torch.cuda.Stream | None = None, out: DeviceMoments | None = None,
+            workspace: torch.Tensor | None = None) -> DeviceMoments:
+    """Whole pipeline (project -> exact 2D moments -> device epilogue).
+
+    ``workspace``: caller-owned uint8 device scratch of at least
+    ``workspace_bytes`` (required for CUDA-graph capture, whose replays keep
+    the pointer); default is the per-thread shared grow-only buffer."""
     check_order(order)
     desc = make_desc(vox, offset, z0)
     check_envelope(desc.L, desc.M, n_global if n_global is not None else desc.N + desc.z0, desc.dtype, order)
@@ -136,7 +150,12 @@ def moments(vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0, n_globa
     wsb = int(lib.dpm_workspace_bytes(ctypes.byref(desc), order))
     if wsb == 0:
         raise ValueError("invalid volume descriptor")
-    ws = _WS.get(wsb, vox.device)
+    if workspace is not None:
+        if workspace.numel() * workspace.element_size() < wsb or workspace.device != vox.device:
+            raise ValueError(f"workspace must hold {wsb} bytes on {vox.device}")
+        ws = workspace
+    else:
+        ws = _WS.get(wsb, vox.device)
     if out is None:
         out = DeviceMoments(
             i128=torch.empty((desc.B, n3d(order), 2), dtype=torch.int64, device=vox.device),
@@ -243,21 +262,64 @@ def ints_to_limbs(values) -> np.ndarray:
 class GraphedMoments:
     """The whole device pipeline for a fixed input tensor, captured once in a
     CUDA graph and replayed (no per-call host work: ctypes calls, tensor-map
-    encoding and launches happen at capture time only)."""
+    encoding and launches happen at capture time only).  Owns its workspace
+    and outputs, so later calls with other shapes cannot move them."""
 
     def __init__(self, vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0, n_global: int | None = None):
         self.vox = vox
         self.order = order
+        self.workspace = torch.empty(workspace_bytes(vox, order, offset, z0), dtype=torch.uint8, device=vox.device)
         self.stream = torch.cuda.Stream(device=vox.device)
         self.stream.wait_stream(torch.cuda.current_stream(vox.device))
+        kw = dict(offset=offset, z0=z0, n_global=n_global, workspace=self.workspace)
         with torch.cuda.stream(self.stream):
-            self.out = moments(vox, order, offset=offset, z0=z0, n_global=n_global)   # warm-up, allocates
+            self.out = moments(vox, order, **kw)   # warm-up, allocates the outputs
             self.launches = self.out.launches
             self.graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(self.graph, stream=self.stream):
-                moments(vox, order, offset=offset, z0=z0, n_global=n_global, out=self.out)
+                moments(vox, order, out=self.out, **kw)
         torch.cuda.current_stream(vox.device).wait_stream(self.stream)
 
     def replay(self) -> DeviceMoments:
         self.graph.replay()
         return self.out
+
+
+class HostGraphedMoments:
+    """Host-buffer entry point for volumes that fit on the device in one piece:
+    pinned host volume -> H2D copy -> project -> 2D moments -> epilogue -> D2H
+    of the exact moments and status into pinned host tensors, all captured in
+    ONE CUDA graph.  ``run()`` replays it and waits; per call the host does one
+    graph launch and one synchronisation."""
+
+    def __init__(self, host: torch.Tensor, order: int, offset: int = 0, device: torch.device | str = "cuda"):
+        if host.device.type != "cpu":
+            raise ValueError("host must be a CPU tensor")
+        self.host = host if host.is_pinned() else host.pin_memory()
+        self.dev = torch.empty(tuple(host.shape), dtype=host.dtype, device=device)
+        self.dev.copy_(self.host)
+        self.inner = GraphedMoments(self.dev, order, offset=offset)   # warm + validates
+        self.i128 = torch.empty(tuple(self.inner.out.i128.shape), dtype=torch.int64, pin_memory=True)
+        self.status = torch.empty(tuple(self.inner.out.status.shape), dtype=torch.int32, pin_memory=True)
+        self.launches = self.inner.launches
+        st = self.inner.stream
+        st.wait_stream(torch.cuda.current_stream(self.dev.device))
+        with torch.cuda.stream(st):
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, stream=st):
+                self.dev.copy_(self.host, non_blocking=True)
+                moments(self.dev, order, offset=offset, out=self.inner.out, workspace=self.inner.workspace)
+                self.i128.copy_(self.inner.out.i128, non_blocking=True)
+                self.status.copy_(self.inner.out.status, non_blocking=True)
+        torch.cuda.current_stream(self.dev.device).wait_stream(st)
+        self.h2d_bytes = self.host.numel() * self.host.element_size()
+        self.d2h_bytes = self.i128.numel() * 8 + self.status.numel() * 4
+
+    def run(self) -> tuple[torch.Tensor, torch.Tensor]:
+        """Re-reads ``host`` (update it in place between calls); returns the
+        pinned (i128 [B, n3d, 2], status [B]) host tensors."""
+        st = self.inner.stream
+        with torch.cuda.stream(st):      # replay() launches on the current stream
+            self.graph.replay()
+        st.synchronize()
+        return self.i128, self.status
