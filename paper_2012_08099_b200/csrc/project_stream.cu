@@ -366,6 +366,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
       if (NI > DPM_IMG_X2P) rc[3].set(g.X0 + 2 * g.Z0, p.s.W[DPM_IMG_X2P]);
       if (NI > DPM_IMG_X2M) rc[4].set(g.X0 - 2 * g.Z0 - 2 * (SZ - 1) + 2 * (p.N - 1), p.s.W[DPM_IMG_X2M]);
     }
+    if (g.zc > 0) {   // warp-uniform: warps past the volume's last plane only join the barrier
     ptx::mbar_wait_addr(full_addr + 8u * cst, cphase);
     const T* tile = reinterpret_cast<const T*>(stages + cst * STAGE_BYTES) + (8 * w) * SX + VX * lane;
 
@@ -481,6 +482,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
         add_halo<G::SOB, VX, N2>(base, wm, lane);
       }
     }
+    }  // g.zc > 0
 
     __syncthreads();
     if (tid == 0 && !prod.done) issue();   // every warp is done with stage `cst`

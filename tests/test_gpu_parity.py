@@ -184,3 +184,34 @@ def test_cfg5_full_volume_exact(cuda):
     want = oracle.dpm(host, 6)
     assert dict(zip(vm.moment_indices(6), _ints(res))) == want
     assert want[(0, 0, 0)] == int(host.sum(dtype=np.uint64))
+
+
+@pytest.mark.parametrize("order", [3, 4, 5, 6])
+def test_derive_exactness_and_nonexact_flag(cuda, order):
+    """Epilogue alone: exact results from a volume's limb accumulator (two
+    volumes per call, one warp each); a +1 on one oblique 2D moment breaks
+    an exact division and must raise DPM_ST_NONEXACT, never a wrong value."""
+    rng = np.random.default_rng(order)
+    vols = rng.integers(0, 65535, size=(2, 13, 11, 17)).astype(np.uint16)
+    acc = engine.moments2d_partial(torch.from_numpy(vols).cuda(), order)
+    res = engine.derive(acc, order)
+    got = res.i128.cpu().numpy()
+    idx = vm.moment_indices(order)
+    for b in range(2):
+        want = oracle.naive(vols[b], order)
+        assert engine.i128_to_ints(got[b]) == [want[k] for k in idx]
+    assert res.status.cpu().tolist() == [0, 0]
+    # perturb DIAG (p=2, q=1) of volume 1: M_{1,1,1} = f/2 becomes non-integral
+    K = order
+    i21 = 2 * (K + 1) - 1 + 1
+    bad = acc.clone()
+    bad[1, 3, i21, 0] += 1
+    st = engine.derive(bad, order).status.cpu().tolist()
+    assert st[0] == 0 and st[1] & 2, st
+    if order >= 5:
+        # perturb X2P (p=4, q=1): the 3-unknown solve's division by 6 fails
+        i41 = 4 * (K + 1) - 4 * 3 // 2 + 1
+        bad = acc.clone()
+        bad[0, 5, i41, 0] += 1
+        st = engine.derive(bad, order).status.cpu().tolist()
+        assert st[0] & 2 and st[1] == 0, st
