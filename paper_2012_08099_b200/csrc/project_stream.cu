@@ -337,13 +337,36 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
   int cst = 0, parity = 0;
   uint32_t cphase = 0;
 
+  // ZX flush at the end of a column segment.  Lane l = 8g + j holds the sums
+  // of x = X0 + VX*l + k, planes t = 0..7.  Per k, an 8x8 shfl.xor butterfly
+  // transposes (lane-in-group, plane) so that afterwards lane j holds plane j of
+  // the 8 x's of its group: every red.global then covers 4 runs of 8
+  // consecutive z (32 B each) instead of 32 scattered words.
   auto flush_zx = [&]() {
     if (col < 0 || DPM_NO_ZX) return;
+    const int j = lane & 7, g8 = lane >> 3;
+    uint32_t* base = p.s.img[DPM_IMG_ZX] + (int64_t)g.b * p.L * p.N + (g.X0 + VX * 8 * g8) * p.N + g.Z0 + 8 * w + j;
+    const bool zok = j < g.zc;
+    const int64_t xg = g.X0 + VX * 8 * g8;
     #pragma unroll
     for (int k = 0; k < VX; ++k) {
+      uint32_t r[8];
       #pragma unroll
-      for (int t = 0; t < 8; ++t)
-        ptx::red_global_add_if(zx_col + k * p.N + t, zx[t][k], zx[t][k] != 0 && g.xok && t < g.zc);
+      for (int t = 0; t < 8; ++t) r[t] = zx[t][k];
+      #pragma unroll
+      for (int sft = 4; sft >= 1; sft >>= 1) {
+        const bool up = (j & sft) != 0;
+        #pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if (t & sft) continue;
+          const uint32_t send = up ? r[t] : r[t | sft];
+          const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, sft);
+          if (up) r[t] = recv; else r[t | sft] = recv;
+        }
+      }
+      #pragma unroll
+      for (int i = 0; i < 8; ++i)   // r[i] = plane j of x = xg + VX*i + k
+        ptx::red_global_add_if(base + (int64_t)(VX * i + k) * p.N, r[i], r[i] != 0 && zok && xg + VX * i + k < p.L);
     }
   };
 
