@@ -211,6 +211,9 @@ template <int NI, int NW, int VX> struct Geo {
   static constexpr int XY = 0, DG = VX * SXY, AN = DG + VX * SOB, XP = AN + VX * SOB, XM = XP + VX * SOB;
   static constexpr int WORDS = NI <= 4 ? DG + VX * SOB : NI == 5 ? AN + VX * SOB : NI == 6 ? XP + VX * SOB : XM + VX * SOB;
   static constexpr int THREADS = 32 * NW;
+  // YZ plane sums staged per 8 consecutive y in shared memory (orders <= 5; at
+  // order 6 the extra code costs more than the scattered atomics it saves)
+  static constexpr int YZT = NI <= 6 ? SZ * 8 : 0;
 };
 
 struct ColGeom {
@@ -287,14 +290,16 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
   constexpr int N1 = VX + 7, N2 = VX + 14;             // oblique window widths
   constexpr bool TWO_PASS = NI >= 6 && VX == 8 && NW > 8;   // +-2z images in a second pass over the stage
   constexpr uint32_t STAGE_BYTES = SX * SZ * sizeof(T);
+  constexpr int YZT = G::YZT;   // words of one YZ tile (0: YZ goes straight to global)
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stages = smem;
   uint32_t* rows = reinterpret_cast<uint32_t*>(smem + STAGES * STAGE_BYTES);   // [2][G::WORDS]
-  uint64_t* full = reinterpret_cast<uint64_t*>(rows + 2 * G::WORDS);           // [STAGES]
+  uint32_t* yzb = rows + 2 * G::WORDS;                                          // [2][SZ][8] plane sums by y % 8
+  uint64_t* full = reinterpret_cast<uint64_t*>(yzb + 2 * YZT);                  // [STAGES]
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t rows_addr = ptx::smem_addr(rows), full_addr = ptx::smem_addr(full);
 
-  for (int i = tid; i < 2 * G::WORDS; i += THREADS) rows[i] = 0;
+  for (int i = tid; i < 2 * G::WORDS + 2 * YZT; i += THREADS) rows[i] = 0;
   if (tid == 0) {
     ptx::prefetch_tmap(&tmap);
     for (int i = 0; i < STAGES; ++i) ptx::mbar_init(&full[i], 1);
@@ -334,7 +339,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
   uint32_t* zx_col = nullptr;
   uint32_t* yz_col = nullptr;
   RegionCol rc[5];
-  int cst = 0, parity = 0;
+  int cst = 0, parity = 0, yzpar = 0;
   uint32_t cphase = 0;
 
   // ZX flush at the end of a column segment.  Lane l = 8g + j holds the sums
@@ -451,7 +456,11 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
       }
       r1 += __shfl_xor_sync(0xffffffffu, r1, 2);
       r1 += __shfl_xor_sync(0xffffffffu, r1, 1);
-      ptx::red_global_add_if(yz_col + y, r1, (lane & 3) == 0 && r1 != 0 && (lane >> 2) < g.zc);
+      if (YZT > 0) {
+        if ((lane & 3) == 0) yzb[yzpar * SZ * 8 + (8 * w + (lane >> 2)) * 8 + (y & 7)] = r1;
+      } else {
+        ptx::red_global_add_if(yz_col + y, r1, (lane & 3) == 0 && r1 != 0 && (lane >> 2) < g.zc);
+      }
     }
 
     // ---- merge window overlaps, add owned cells (and the tile's halo) into the CTA rows
@@ -529,6 +538,21 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     parity ^= 1;
     if (++cst == STAGES) { cst = 0; cphase ^= 1u; }
     cur.advance(p);
+    // YZ tile -> image once 8 consecutive y are in (or the run of y breaks):
+    // 8 threads cover 32 contiguous bytes of a z-row
+    if (YZT > 0 && (cur.done || cur.c != col || cur.y() != y + 1 || ((y + 1) & 7) == 0)) {
+      uint32_t* tb = yzb + yzpar * SZ * 8;
+      uint32_t* gy = p.s.img[DPM_IMG_YZ] + (int64_t)g.b * p.M * p.N + g.Z0 * p.M + (y & ~7);
+      #pragma unroll
+      for (int it = 0; it < (SZ * 8 + THREADS - 1) / THREADS; ++it) {
+        const int i = tid + it * THREADS;
+        if ((SZ * 8) % THREADS != 0 && i >= SZ * 8) break;
+        const uint32_t v = tb[i];
+        tb[i] = 0;
+        ptx::red_global_add_if(gy + (int64_t)(i >> 3) * p.M + (i & 7), v, v != 0);
+      }
+      yzpar ^= 1;
+    }
   }
   flush_zx();
 }
@@ -578,7 +602,7 @@ template <int NI, int VX> struct WarpsFor {
 template <typename T, int NI, int VX> struct StagesFor {
   static constexpr int NW = WarpsFor<NI, VX>::value;
   static constexpr int BOX = 32 * VX * 8 * NW * (int)sizeof(T);
-  static constexpr int ROWS = 2 * Geo<NI, NW, VX>::WORDS * 4;
+  static constexpr int ROWS = 2 * Geo<NI, NW, VX>::WORDS * 4 + 2 * Geo<NI, NW, VX>::YZT * 4;
   static constexpr int FIT = (220 * 1024 - ROWS) / BOX;
   static constexpr int value = FIT > 12 ? 12 : FIT;
 };
@@ -588,7 +612,7 @@ static int launch_one(const dpm_volume_desc* d, const void* vox, int grid, cudaS
   constexpr int NW = WarpsFor<NI, VX>::value;
   constexpr int S = StagesFor<T, NI, VX>::value;
   using G = Geo<NI, NW, VX>;
-  constexpr size_t bytes = (size_t)S * G::SX * G::SZ * sizeof(T) + 2 * G::WORDS * 4 + S * 8;
+  constexpr size_t bytes = (size_t)S * G::SX * G::SZ * sizeof(T) + 2 * G::WORDS * 4 + 2 * G::YZT * 4 + S * 8;
   static_assert(bytes <= 227 * 1024, "shared memory budget");
   const int64_t es = sizeof(T);
   CUtensorMap map;
