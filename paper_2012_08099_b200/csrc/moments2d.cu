@@ -22,6 +22,7 @@
 namespace dpm {
 
 constexpr int M2_THREADS = 128;
+constexpr int M2_CHUNK = 8;   // moments per stage-2 reduction round (4 * M2_CHUNK == M2_THREADS / 4)
 
 template <int JB> struct Limbs {
   __host__ __device__ static constexpr int nl(int q) { return q == 0 ? 1 : (q * JB + 23) / 24; }
@@ -98,38 +99,57 @@ __global__ void __launch_bounds__(M2_THREADS) moments2d_kernel(M2Params p) {
   }
 
   __syncthreads();  // table dead from here on; its storage becomes red
-  // stage 2: C_q (mod 2^128) times (i + ai)^p, p + q <= K
+  // stage 2: C_q (mod 2^128) times (i + ai)^p, p + q <= K, reduced over the
+  // CTA's columns M2_CHUNK moments at a time (keeps the shared buffer small,
+  // so occupancy is set by the 16 KB row table, not by the reduction)
   unsigned __int128 C[K + 1];
   #pragma unroll
   for (int q = 0; q <= K; ++q) {
     unsigned __int128 c = 0;
     #pragma unroll
     for (int l = 0; l < LP::nl(q); ++l) c += ((unsigned __int128)acc[LP::off(q) + l]) << (24 * l);
-    C[q] = c;
+    C[q] = (i < W) ? c : 0;
   }
-  const __int128 x = (__int128)(i + ai);
-  __int128 xp = 1;
-  int m = 0;
-  #pragma unroll
-  for (int pp = 0; pp <= K; ++pp) {
+  unsigned __int128 xp[K + 1];
+  {
+    const __int128 x = (__int128)(i + ai);
+    __int128 t = 1;
     #pragma unroll
-    for (int q = 0; q <= K - pp; ++q) {
-      unsigned __int128 v = (i < W) ? C[q] * (unsigned __int128)xp : 0;
-      red[4 * m + 0][tid] = (uint32_t)v;
-      red[4 * m + 1][tid] = (uint32_t)(v >> 32);
-      red[4 * m + 2][tid] = (uint32_t)(v >> 64);
-      red[4 * m + 3][tid] = (uint32_t)(v >> 96);
-      ++m;
-    }
-    xp *= x;
+    for (int pp = 0; pp <= K; ++pp) { xp[pp] = (unsigned __int128)t; t *= x; }
   }
-  __syncthreads();
   uint64_t* out = p.acc + ((b * p.s.n_img + k) * N2) * 4;
-  for (int e = tid; e < N2 * 4; e += M2_THREADS) {
-    uint64_t s = 0;
-    #pragma unroll 8
-    for (int t = 0; t < M2_THREADS; ++t) s += red[e][t];
-    if (s) atomicAdd(reinterpret_cast<unsigned long long*>(out + e), (unsigned long long)s);
+  #pragma unroll
+  for (int m0 = 0; m0 < N2; m0 += M2_CHUNK) {
+    int m = 0;
+    #pragma unroll
+    for (int pp = 0; pp <= K; ++pp) {
+      #pragma unroll
+      for (int q = 0; q <= K - pp; ++q, ++m) {
+        if (m < m0 || m >= m0 + M2_CHUNK) continue;
+        const unsigned __int128 v = C[q] * xp[pp];
+        const int e = m - m0;
+        red[4 * e + 0][tid] = (uint32_t)v;
+        red[4 * e + 1][tid] = (uint32_t)(v >> 32);
+        red[4 * e + 2][tid] = (uint32_t)(v >> 64);
+        red[4 * e + 3][tid] = (uint32_t)(v >> 96);
+      }
+    }
+    __syncthreads();
+    // 4 threads per limb row: 32 columns each, then a 4-lane shuffle sum
+    {
+      const int e = tid >> 2, part = tid & 3;
+      uint64_t sum = 0;
+      if (e < 4 * M2_CHUNK) {
+        #pragma unroll 8
+        for (int t = part * 32; t < part * 32 + 32; ++t) sum += red[e][t];
+      }
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      const int gm = m0 + (e >> 2);
+      if (part == 0 && e < 4 * M2_CHUNK && gm < N2 && sum)
+        atomicAdd(reinterpret_cast<unsigned long long*>(out + 4 * m0 + e), (unsigned long long)sum);
+    }
+    __syncthreads();
   }
 }
 
@@ -138,7 +158,7 @@ static void launch_kj(dim3 grid, cudaStream_t st, const M2Params& p) {
   constexpr int NT = Limbs<JB>::off(K + 1);
   constexpr int NTP = (NT + 3) & ~3;
   constexpr int N2 = (K + 1) * (K + 2) / 2;
-  constexpr size_t t_bytes = 256 * NTP * 4, r_bytes = (size_t)N2 * 4 * (M2_THREADS + 1) * 4;
+  constexpr size_t t_bytes = 256 * NTP * 4, r_bytes = (size_t)M2_CHUNK * 4 * (M2_THREADS + 1) * 4;
   constexpr size_t bytes = t_bytes > r_bytes ? t_bytes : r_bytes;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -157,10 +177,16 @@ static void launch_k(int jb, dim3 grid, cudaStream_t st, const M2Params& p) {
 int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_t* acc, cudaStream_t st) {
   M2Params p;
   p.s = s; p.B = B; p.acc = acc;
-  // rows per chunk: fewer rows -> more CTAs for short images
-  int64_t px = 0, maxH = 0;
-  for (int k = 0; k < s.n_img; ++k) { px += s.W[k] * s.H[k]; maxH = s.H[k] > maxH ? s.H[k] : maxH; }
-  p.rc = (px * B < (int64_t)(1 << 22)) ? 64 : 256;
+  // rows per chunk: the largest of 256/128/64 that still gives >= 8 CTAs per SM
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  p.rc = 64;
+  for (int64_t rc = 256; rc >= 128; rc >>= 1) {
+    int64_t nb = 0;
+    for (int k = 0; k < s.n_img; ++k) nb += ((s.W[k] + M2_THREADS - 1) / M2_THREADS) * ((s.H[k] + rc - 1) / rc);
+    if (nb * B >= 8 * (int64_t)sms) { p.rc = rc; break; }
+  }
   p.blocks_img[0] = 0;
   for (int k = 0; k < s.n_img; ++k) {
     p.cblocks[k] = (s.W[k] + M2_THREADS - 1) / M2_THREADS;

@@ -5,7 +5,7 @@ for rep in 1 2; do
   for v in A B; do
     cp tools/ab/$v.so paper_2012_08099_b200/libdpm_b200.so
     for c in "${CS[@]}"; do
-      t=$(ncu --metrics gpu__time_duration.sum --clock-control none -k regex:project_stream -c 3 --csv python tools/time_project.py "$c" 2>/dev/null | grep project_stream | tail -1 | rev | cut -d, -f1 | rev)
+      t=$(ncu --metrics gpu__time_duration.sum --clock-control none -k regex:${KREGEX:-project_stream} -c 3 --csv python tools/time_project.py "$c" 2>/dev/null | grep ${KREGEX:-project_stream} | tail -1 | rev | cut -d, -f1 | rev)
       echo "$rep $v $c $t"
     done
   done
