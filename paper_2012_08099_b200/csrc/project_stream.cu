@@ -291,6 +291,13 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
   constexpr bool TWO_PASS = NI >= 6 && VX == 8 && NW > 8;   // +-2z images in a second pass over the stage
   constexpr uint32_t STAGE_BYTES = SX * SZ * sizeof(T);
   constexpr int YZT = G::YZT;   // words of one YZ tile (0: YZ goes straight to global)
+  // TMA producer: lane 0 of a middle warp.  The row flushes start at thread 0,
+  // so warps 0-3 carry them; keeping the producer's per-row-step work off those
+  // warps shortens the slowest warp (cfg5 -5.7 %, tools/EXPERIMENTS.md v14)
+  // TMA producer: lane 0 of a middle warp.  The row flushes start at thread 0,
+  // so warps 0-3 carry them; keeping the producer's per-row-step work off those
+  // warps shortens the slowest warp (cfg5 -5.7 %, tools/EXPERIMENTS.md v14)
+  constexpr int PROD = 32 * (NW / 2);
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stages = smem;
   uint32_t* rows = reinterpret_cast<uint32_t*>(smem + STAGES * STAGE_BYTES);   // [2][G::WORDS]
@@ -321,7 +328,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     prod.advance(p);
     if (++pst == STAGES) pst = 0;
   };
-  if (tid == 0) {
+  if (tid == PROD) {
     evict_first = ptx::policy_evict_first();
     prod.init(p);
     for (int i = 0; i < STAGES && !prod.done; ++i) issue();
@@ -517,7 +524,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     }  // g.zc > 0
 
     __syncthreads();
-    if (tid == 0 && !prod.done) issue();   // every warp is done with stage `cst`
+    if (tid == PROD && !prod.done) issue();   // every warp is done with stage `cst`
 
     // ---- flush this row-step's CTA rows -------------------------------------
     {
@@ -543,9 +550,10 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     if (YZT > 0 && (cur.done || cur.c != col || cur.y() != y + 1 || ((y + 1) & 7) == 0)) {
       uint32_t* tb = yzb + yzpar * SZ * 8;
       uint32_t* gy = p.s.img[DPM_IMG_YZ] + (int64_t)g.b * p.M * p.N + g.Z0 * p.M + (y & ~7);
+      const int ty = tid;   // (spreading the flushes over all warps measured slower: 4 %)
       #pragma unroll
       for (int it = 0; it < (SZ * 8 + THREADS - 1) / THREADS; ++it) {
-        const int i = tid + it * THREADS;
+        const int i = ty + it * THREADS;
         if ((SZ * 8) % THREADS != 0 && i >= SZ * 8) break;
         const uint32_t v = tb[i];
         tb[i] = 0;
