@@ -115,6 +115,17 @@ DPM_API int dpm_project(const dpm_volume_desc* desc, const void* d_voxels, int n
 DPM_API int dpm_moments2d(const dpm_volume_desc* desc, int n_img, const uint32_t* const* d_images,
                   int order, uint64_t* d_acc, void* stream);
 
+/* Exact 2D raw moments of ONE stand-alone device image, pixels[j][i]
+ * (contiguous rows of W uint32), about additive origins (ai, aj >= 0):
+ *   M_pq = sum_{i,j} I[j][i] (i + ai)^p (j + aj)^q,  p + q <= order (3..6).
+ * Replaces drt2d.brute_force_2d and assemble_2d(integrals(image))
+ * (drt2d.py:140-193) for device images: same values, any order up to 6.
+ * d_acc: n2d(order) * 4 uint64 limb sums, zeroed by the call (read as in
+ * dpm_moments2d).  The caller checks the exactness envelope
+ * (mass * max|coordinate|^order < 2^126); DPM_EOVERFLOW if H - 1 + aj >= 2^21. */
+DPM_API int dpm_image_moments2d(const uint32_t* d_pixels, int64_t W, int64_t H, int64_t ai, int64_t aj,
+                                int order, uint64_t* d_acc, void* stream);
+
 /* Device epilogue: placement + duplicate-route checks + cross-axis solve.
  * Replaces moments3d._place / _cross_axis_moments / dpm_moments:255-264
  * (moments3d.py:201-264).  Reads d_acc (as written by dpm_moments2d), writes

@@ -6,7 +6,9 @@ moments, with every stage running in hand-written sm_100a CUDA kernels behind
 the C ABI in include/dpm_b200.h.  There is no CPU fallback: without the CUDA
 library (paper_2012_08099_b200/libdpm_b200.so) and a GPU, compute calls raise.
 """
+from . import drt2d
 from .counters import OpCounters
+from .drt2d import Moments2D, brute_force_2d, image_moments, shift_origin
 from .errors import FormatError, InconsistencyError
 from .moments3d import (ENGINES, MomentTensor3, count_ops, dpm_moments, dpm_moments_batch,
                         moment_indices)
@@ -17,8 +19,9 @@ from .volume import Volume, delta, ellipsoid, random, uniform
 __version__ = "0.1.0"
 
 __all__ = [
-    "ANGLES", "ENGINES", "FormatError", "InconsistencyError", "MomentTensor3", "OpCounters",
+    "ANGLES", "ENGINES", "FormatError", "InconsistencyError", "Moments2D", "MomentTensor3", "OpCounters",
     "Orientation", "ProjectionImage", "ProjectionSet", "Volume", "count_ops", "delta",
-    "dpm_moments", "dpm_moments_batch", "ellipsoid", "moment_indices", "project", "project_all",
-    "project_extended", "project_subset", "random", "uniform", "write_pgm",
+    "brute_force_2d", "dpm_moments", "dpm_moments_batch", "drt2d", "ellipsoid", "image_moments",
+    "moment_indices", "project", "project_all",
+    "project_extended", "project_subset", "random", "shift_origin", "uniform", "write_pgm",
 ]

@@ -25,7 +25,7 @@ EXPORTS = (
     "dpm_num_images", "dpm_num_moments3d", "dpm_num_moments2d", "dpm_image_layout",
     "dpm_project_workspace_bytes", "dpm_project", "dpm_moments2d", "dpm_derive3d",
     "dpm_workspace_bytes", "dpm_moments", "dpm_check_envelope", "dpm_acc_add",
-    "dpm_synth_noise_u16", "dpm_last_launch_count", "dpm_strerror",
+    "dpm_synth_noise_u16", "dpm_last_launch_count", "dpm_strerror", "dpm_image_moments2d",
 )
 
 
@@ -64,6 +64,7 @@ def lib() -> ctypes.CDLL:
         "dpm_project": (ctypes.c_int, [pdesc, vp, ctypes.c_int, ctypes.POINTER(vp), vp, sz, vp]),
         "dpm_moments2d": (ctypes.c_int, [pdesc, ctypes.c_int, ctypes.POINTER(vp), ctypes.c_int, vp, vp]),
         "dpm_derive3d": (ctypes.c_int, [pdesc, vp, ctypes.c_int, vp, vp, vp, vp]),
+        "dpm_image_moments2d": (ctypes.c_int, [vp, i64, i64, i64, i64, ctypes.c_int, vp, vp]),
         "dpm_workspace_bytes": (sz, [pdesc, ctypes.c_int]),
         "dpm_moments": (ctypes.c_int, [pdesc, vp, ctypes.c_int, vp, sz, vp, vp, vp, vp]),
         "dpm_check_envelope": (ctypes.c_int, [i64, i64, i64, i64, ctypes.c_int]),

@@ -131,6 +131,22 @@ int dpm_moments2d(const dpm_volume_desc* desc, int n_img, const uint32_t* const*
   return launch_moments2d(s, desc->B, order, jb, d_acc, st);
 }
 
+int dpm_image_moments2d(const uint32_t* d_pixels, int64_t W, int64_t H, int64_t ai, int64_t aj, int order,
+                        uint64_t* d_acc, void* stream) {
+  reset_launches();
+  if (!d_pixels || !d_acc || W < 1 || H < 1 || aj < 0 || check_order(order)) return DPM_EINVAL;
+  int jb = 0;
+  while ((int64_t(1) << jb) <= H - 1 + aj) ++jb;
+  if (jb > 21) return DPM_EOVERFLOW;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ImageSet s{};
+  s.n_img = 1;
+  s.img[0] = const_cast<uint32_t*>(d_pixels);
+  s.W[0] = W; s.H[0] = H; s.ai[0] = ai; s.aj[0] = aj;
+  if (cudaMemsetAsync(d_acc, 0, (size_t)n2d(order) * 4 * sizeof(uint64_t), st) != cudaSuccess) return DPM_ECUDA;
+  return launch_moments2d(s, 1, order, jb, d_acc, st);
+}
+
 int dpm_derive3d(const dpm_volume_desc* desc, const uint64_t* d_acc, int order, int64_t* d_m3d_i128,
                  double* d_m3d_f64, int32_t* d_status, void* stream) {
   reset_launches();

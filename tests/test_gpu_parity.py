@@ -215,3 +215,37 @@ def test_derive_exactness_and_nonexact_flag(cuda, order):
         bad[0, 5, i41, 0] += 1
         st = engine.derive(bad, order).status.cpu().tolist()
         assert st[0] & 2 and st[1] == 0, st
+
+
+@pytest.mark.parametrize("order", [0, 2, 3, 4, 6])
+def test_image_moments_2d(cuda, order):
+    """Device 2D moments of stand-alone images == the direct definition
+    (stored coordinates, origin carried) and, after shift_origin, the moments
+    about the logical origin (ANTI's N-1)."""
+    rng = np.random.default_rng(40 + order)
+    px = rng.integers(0, 2**32, size=(7, 13), dtype=np.uint64)
+    got = vm.image_moments(px, order)
+    want = {(p, q): sum(int(px[j, i]) * i ** p * j ** q for j in range(7) for i in range(13))
+            for p in range(order + 1) for q in range(order + 1 - p)}
+    assert got.values == want and got.order == order
+    v = vm.random((6, 5, 4), 16, seed=order)
+    anti = vm.project(v, vm.Orientation.ANTI)
+    m = vm.shift_origin(vm.brute_force_2d(anti, max(order, 1)), anti.origin_offset)
+    n = v.dims[2]
+    logical = {}
+    vox = v.voxels.astype(object)
+    for p in range(max(order, 1) + 1):
+        for q in range(max(order, 1) + 1 - p):
+            logical[(p, q)] = sum(vox[z, y, x] * (x - z) ** p * y ** q for z in range(n) for y in range(5) for x in range(6))
+    assert m.values == logical
+
+
+def test_image_moments_2d_errors(cuda):
+    with pytest.raises(ValueError):
+        vm.image_moments(np.zeros((3, 3, 3)), 3)
+    with pytest.raises(ValueError):
+        vm.image_moments(np.full((3, 3), -1), 3)
+    with pytest.raises(ValueError):
+        vm.image_moments(np.ones((3, 3)), 7)
+    with pytest.raises(OverflowError):
+        vm.image_moments(np.full((4000, 4000), 2**32 - 1, dtype=np.uint64), 6)

@@ -83,3 +83,32 @@ def test_compute_calls_fail_loudly_without_cuda():
         pytest.skip("has a GPU")
     with pytest.raises(Exception):
         vm.dpm_moments(vm.uniform((2, 2, 2), 1), 3)
+
+
+def _brute2d(px, order, x0=0):
+    """Pure-Python 2D moments about first-axis origin x0 (test restatement of
+    the reference's direct definition, drt2d.py:177-193)."""
+    h, w = px.shape
+    out = {}
+    for p in range(order + 1):
+        for q in range(order + 1 - p):
+            out[(p, q)] = sum(int(px[j, i]) * (i - x0) ** p * j ** q for j in range(h) for i in range(w))
+    return out
+
+
+def test_shift_origin_matches_direct_definition():
+    from paper_2012_08099_b200.drt2d import Moments2D, shift_origin
+    rng = np.random.default_rng(4)
+    px = rng.integers(0, 1000, size=(5, 9))
+    for order, off in [(3, 2), (4, 8), (6, 3)]:
+        m = Moments2D(order, _brute2d(px, order), origin_offset=off)
+        sh = shift_origin(m, off)
+        assert sh.origin_offset == 0 and sh.order == order
+        assert sh.values == _brute2d(px, order, x0=off)
+        assert shift_origin(m, 0).values == m.values
+
+
+def test_moments2d_type_mirrors_reference():
+    from paper_2012_08099_b200.drt2d import Moments2D
+    m = Moments2D(3, {(0, 0): 7, (1, 0): 3}, 2)
+    assert m[(1, 0)] == 3 and m.mass == 7 and m.origin_offset == 2
