@@ -11,9 +11,10 @@ from .counters import OpCounters
 from .drt2d import Moments2D, brute_force_2d, image_moments, shift_origin
 from .errors import FormatError, InconsistencyError
 from .moments3d import (ENGINES, MomentTensor3, count_ops, dpm_moments, dpm_moments_batch,
-                        moment_indices)
+                        dpm_moments_file, moment_indices)
 from .projection import (ANGLES, Orientation, ProjectionImage, ProjectionSet, project, project_all,
                          project_extended, project_subset, write_pgm)
+from .volio import VolumeMeta, load_nrrd, load_raw, meta_from_header_file, open_nrrd, open_raw, write_raw
 from .volume import Volume, delta, ellipsoid, random, uniform
 
 __version__ = "0.1.0"
@@ -21,7 +22,8 @@ __version__ = "0.1.0"
 __all__ = [
     "ANGLES", "ENGINES", "FormatError", "InconsistencyError", "Moments2D", "MomentTensor3", "OpCounters",
     "Orientation", "ProjectionImage", "ProjectionSet", "Volume", "count_ops", "delta",
-    "brute_force_2d", "dpm_moments", "dpm_moments_batch", "drt2d", "ellipsoid", "image_moments",
+    "VolumeMeta", "brute_force_2d", "dpm_moments", "dpm_moments_batch", "dpm_moments_file", "drt2d",
+    "ellipsoid", "image_moments", "load_nrrd", "load_raw", "meta_from_header_file", "open_nrrd", "open_raw",
     "moment_indices", "project", "project_all",
-    "project_extended", "project_subset", "random", "shift_origin", "uniform", "write_pgm",
+    "project_extended", "project_subset", "random", "shift_origin", "uniform", "write_pgm", "write_raw",
 ]

@@ -102,6 +102,37 @@ def dpm_moments(volume: Volume, order: int, counters: OpCounters | None = None,
     return MomentTensor3(order, dict(zip(moment_indices(order), vals)))
 
 
+def dpm_moments_file(source, order: int, meta=None, chunk_planes: int = 64, counters: OpCounters | None = None,
+                     check_consistency: bool = True) -> MomentTensor3:
+    """``dpm_moments`` of a volume file streamed slab by slab (SURVEY.md §8(f)
+    row 1): ``source`` is a raw path (with ``meta``, a ``VolumeMeta``), an
+    NRRD path, or a ``Volume`` (e.g. memory-mapped).  The volume never has to
+    fit in host or device memory; results are identical to ``dpm_moments``."""
+    import torch
+
+    from . import engine, volio
+    from .streaming import FileStreamer
+
+    engine.check_order(order)
+    if isinstance(source, Volume):
+        vol = source
+    elif meta is not None:
+        vol = volio.open_raw(source, meta)
+    else:
+        vol = volio.open_nrrd(source)
+    l, m, n = vol.dims
+    engine.check_envelope(l, m, n, nat.DPM_U8 if vol.bit_depth == 8 else nat.DPM_U16, order)
+    fs = FileStreamer((n, m, l), vol.voxels.dtype, order, chunk_planes=chunk_planes)
+    res = fs.moments(vol.voxels)
+    torch.cuda.current_stream().synchronize()
+    st = int(res.status[0].item())
+    if check_consistency:
+        raise_status(st)
+    vals = engine.i128_to_ints(res.i128[0].cpu().numpy())
+    _count(counters, order, vol.dims)
+    return MomentTensor3(order, dict(zip(moment_indices(order), vals)))
+
+
 def dpm_moments_batch(volumes, order: int, check_consistency: bool = True, offset: int = 0,
                       as_float: bool = False):
     """Moments of a batch of equally shaped volumes ([B, N, M, L] numpy or torch).

@@ -69,3 +69,58 @@ class HostStreamer:
         res = engine.derive(acc, self.order)
         self.launches += 1
         return res
+
+
+class FileStreamer:
+    """Moments of a volume that lives in a file (or any host array, e.g. a
+    read-only ``np.memmap`` from ``volio.open_raw`` / ``open_nrrd``) and need
+    not fit in host or device memory: a three-stage pipeline per z-slab of
+    ``chunk_planes`` planes -- file pages -> pinned staging (host copy, which
+    is where the disk read happens) -> device buffer (copy stream) ->
+    projection + exact 2D moments in global coordinates (compute stream).  The
+    host fills slab k+1 while the device copies / reduces slab k; the
+    per-slab limb accumulators add exactly and the epilogue runs once."""
+
+    def __init__(self, shape_nml, dtype, order: int, chunk_planes: int = 64, device=None):
+        import numpy as np
+
+        engine.check_order(order)
+        self.N, self.M, self.L = shape_nml
+        self.order = order
+        self.chunk = max(1, min(chunk_planes, self.N))
+        self.device = torch.device(device or "cuda")
+        tdt = {np.dtype("uint8"): torch.uint8, np.dtype("uint16"): torch.uint16}[np.dtype(dtype)]
+        self.staging = [torch.empty((self.chunk, self.M, self.L), dtype=tdt, pin_memory=True) for _ in range(2)]
+        self.staging_np = [s.numpy() for s in self.staging]
+        self.bufs = [torch.empty((self.chunk, self.M, self.L), dtype=tdt, device=self.device) for _ in range(2)]
+        self.copy_stream = torch.cuda.Stream(device=self.device)
+        self.copied = [torch.cuda.Event() for _ in range(2)]
+        self.consumed = [torch.cuda.Event() for _ in range(2)]
+        n_img = engine.num_images(order)
+        self.acc_total = torch.zeros((1, n_img, engine.n2d(order), 4), dtype=torch.int64, device=self.device)
+        self.bytes_read = 0
+
+    def run(self, src) -> torch.Tensor:
+        """Limb accumulator of the 2D moments of ``src`` ([N, M, L] array)."""
+        assert tuple(src.shape) == (self.N, self.M, self.L)
+        comp = torch.cuda.current_stream(self.device)
+        self.acc_total.zero_()
+        self.bytes_read = 0
+        for k, z0 in enumerate(range(0, self.N, self.chunk)):
+            z1 = min(self.N, z0 + self.chunk)
+            i = k % 2
+            self.copied[i].synchronize()                       # staging[i]'s previous H2D is done
+            self.staging_np[i][: z1 - z0] = src[z0:z1]         # file -> pinned (the disk read)
+            self.bytes_read += self.staging_np[i][: z1 - z0].nbytes
+            with torch.cuda.stream(self.copy_stream):
+                self.copy_stream.wait_event(self.consumed[i])  # bufs[i]'s previous slab is reduced
+                self.bufs[i][: z1 - z0].copy_(self.staging[i][: z1 - z0], non_blocking=True)
+                self.copied[i].record(self.copy_stream)
+            comp.wait_event(self.copied[i])
+            acc = engine.moments2d_partial(self.bufs[i][: z1 - z0], self.order, z0=z0)
+            engine.acc_add(self.acc_total, acc)
+            self.consumed[i].record(comp)
+        return self.acc_total
+
+    def moments(self, src):
+        return engine.derive(self.run(src), self.order)
