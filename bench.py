@@ -289,16 +289,31 @@ def main():
     torch.cuda.synchronize()
     launches[0] = 0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l2 = int(getattr(torch.cuda.get_device_properties(dev), "L2_cache_size", 126 << 20) or (126 << 20))
+    flush_l2 = my_bytes <= l2
     with ClockSampler(local) as clk:
-        e0.record(stream)
-        for i in range(args.steps):
-            res = step(i)
-        e1.record(stream)
-        torch.cuda.synchronize()
+        if flush_l2:
+            # input fits in L2: scrub L2 (untimed write of 2x its size) before
+            # every step and time each step with its own event pair
+            scrub = torch.empty(2 * l2 // 4, dtype=torch.int32, device=dev)
+            es = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+            ee = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+            for i in range(args.steps):
+                scrub.fill_(i)
+                es[i].record(stream)
+                res = step(i)
+                ee[i].record(stream)
+            torch.cuda.synchronize()
+        else:
+            e0.record(stream)
+            for i in range(args.steps):
+                res = step(i)
+            e1.record(stream)
+            torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
+    ms = sum(a.elapsed_time(b) for a, b in zip(es, ee)) if flush_l2 else e0.elapsed_time(e1)
     proj_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev_p0, ev_p1))
     st = res.status.cpu()
     if int(st.max().item()) != 0:
@@ -339,8 +354,8 @@ def main():
         "scaling": scaling, "vs_baseline": None, "dtype": "u16" if vox.element_size() == 2 else "u8",
         "data": "synthetic (seeded; BASELINE.json configs, see paper_2012_08099_b200/synth.py)",
         "config": {"workload": CONFIG_DESC[cfg], "order": order, "parallelism": parallelism,
-                   "voxels_per_step": total_voxels, "cache": "inputs larger than L2 (no flush)" if my_bytes > (126 << 20)
-                   else "input fits L2: each step re-reads it (warm L2)"},
+                   "voxels_per_step": total_voxels, "cache": "L2 scrubbed before every step (untimed 2xL2 write), per-step events"
+                   if flush_l2 else "inputs larger than L2 (no flush)"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
                      "kernel": "project_stream (projection stage incl. image zeroing)" if cfg == 5 else "whole pipeline",
