@@ -10,6 +10,8 @@ from . import drt2d
 from .counters import OpCounters
 from .drt2d import Moments2D, brute_force_2d, image_moments, shift_origin
 from .errors import FormatError, InconsistencyError
+from .features import (CentralMoments3, ShapeFeatures, apply_spacing, central_moments, centroid, feature_report,
+                       normalize_scale, shape_features)
 from .moments3d import (ENGINES, MomentTensor3, count_ops, dpm_moments, dpm_moments_batch,
                         dpm_moments_file, moment_indices)
 from .projection import (ANGLES, Orientation, ProjectionImage, ProjectionSet, project, project_all,
@@ -20,7 +22,8 @@ from .volume import Volume, delta, ellipsoid, random, uniform
 __version__ = "0.1.0"
 
 __all__ = [
-    "ANGLES", "ENGINES", "FormatError", "InconsistencyError", "Moments2D", "MomentTensor3", "OpCounters",
+    "ANGLES", "CentralMoments3", "ENGINES", "FormatError", "ShapeFeatures", "apply_spacing", "central_moments",
+    "centroid", "feature_report", "normalize_scale", "shape_features", "InconsistencyError", "Moments2D", "MomentTensor3", "OpCounters",
     "Orientation", "ProjectionImage", "ProjectionSet", "Volume", "count_ops", "delta",
     "VolumeMeta", "brute_force_2d", "dpm_moments", "dpm_moments_batch", "dpm_moments_file", "drt2d",
     "ellipsoid", "image_moments", "load_nrrd", "load_raw", "meta_from_header_file", "open_nrrd", "open_raw",
