@@ -128,21 +128,6 @@ __device__ __forceinline__ void fold_pair(uint32_t* win, const uint32_t* a, cons
   }
 }
 
-// Window cell c >= VX belongs to lane + c/VX (slot c % VX): shuffle up and add
-// (predicated on the source lane existing).  Cells [VX, NW) stay intact for the
-// halo reductions of the top lanes.
-template <int NW, int VX>
-__device__ __forceinline__ void merge_owned(uint32_t* win, const uint32_t* mk) {
-  // all shuffles first, then the adds: the shuffle latencies overlap.  shfl.up
-  // hands lanes below the shift their own value; mk[d] = (lane >= d) zeroes it
-  // inside one IMAD (FMA pipe) instead of a select plus an add.
-  uint32_t in[NW];
-  #pragma unroll
-  for (int c = VX; c < NW; ++c) in[c] = __shfl_up_sync(0xffffffffu, win[c], c / VX);
-  #pragma unroll
-  for (int c = VX; c < NW; ++c) win[c % VX] = ptx::mad_u32(in[c], mk[c / VX], win[c % VX]);
-}
-
 // owned cells VX*g .. VX*g+VX-1 of a transposed region with stride S: word c*S + g;
 // `addr` = region byte address + 4*g
 template <int S, int VX>
@@ -151,12 +136,14 @@ __device__ __forceinline__ void add_owned(uint32_t addr, const uint32_t* win) {
   for (int c = 0; c < VX; ++c) ptx::red_shared_add_dyn(addr + 4 * c * S, win[c]);
 }
 
-// halo: window cells whose owner lane would be >= 32 (next x-tile) go straight into the CTA row
+// whole window: cell c of lane g goes to word (c % VX) * S + g + c / VX --
+// for a fixed c the 32 lanes hit 32 consecutive words (no bank conflict);
+// overlaps between neighbouring lanes and the top lanes' halo are resolved
+// by the shared-memory atomics themselves (no shuffles, no per-lane branches)
 template <int S, int VX, int NW>
-__device__ __forceinline__ void add_halo(uint32_t addr, const uint32_t* win, int lane) {
+__device__ __forceinline__ void add_window(uint32_t addr, const uint32_t* win) {
   #pragma unroll
-  for (int c = VX; c < NW; ++c)
-    if (lane + c / VX >= 32) ptx::red_shared_add_dyn(addr + 4 * ((c % VX) * S + c / VX), win[c]);
+  for (int c = 0; c < NW; ++c) ptx::red_shared_add_dyn(addr + 4 * ((c % VX) * S + c / VX), win[c]);
 }
 
 // VX-value sums with 3-input adds
@@ -353,9 +340,6 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     }
   };
 
-  uint32_t mk[N2 / VX + 1];   // mk[d] = 1 where lane d below exists (window merges)
-  #pragma unroll
-  for (int d = 0; d <= N2 / VX; ++d) mk[d] = lane >= d ? p.one : 0u;
   Cursor cur;
   cur.init(p);
   uint32_t zx[8][VX];
@@ -490,22 +474,16 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     }
 
     // ---- merge window overlaps, add owned cells (and the tile's halo) into the CTA rows
-    merge_owned<N1, VX>(wd, mk);
-    if (NI > DPM_IMG_ANTI) merge_owned<N1, VX>(wa, mk);
-    if (!TWO_PASS && NI > DPM_IMG_X2P) merge_owned<N2, VX>(wp, mk);
-    if (!TWO_PASS && NI > DPM_IMG_X2M) merge_owned<N2, VX>(wm, mk);
     {
       const uint32_t rp = rows_addr + (uint32_t)(parity * G::WORDS * 4);
       add_owned<G::SXY, VX>(rp + 4 * (G::XY + lane), cs);
       {
         const uint32_t base = rp + 4 * (G::DG + lane + (8 / VX) * w);
-        add_owned<G::SOB, VX>(base, wd);
-        add_halo<G::SOB, VX, N1>(base, wd, lane);
+        add_window<G::SOB, VX, N1>(base, wd);
       }
       if (NI > DPM_IMG_ANTI) {
         const uint32_t base = rp + 4 * (G::AN + lane + (8 / VX) * (NW - 1 - w));
-        add_owned<G::SOB, VX>(base, wa);
-        add_halo<G::SOB, VX, N1>(base, wa, lane);
+        add_window<G::SOB, VX, N1>(base, wa);
       }
       if (TWO_PASS) {
         // second pass over the same stage for the (x +- 2z, y) images: keeps the
@@ -526,18 +504,14 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
           fold_pair<N2, VX>(wp, a, bb, 2 * t0, 2 * t0 + 2);
           fold_pair<N2, VX>(wm, a, bb, 14 - 2 * t0, 12 - 2 * t0);
         }
-        merge_owned<N2, VX>(wp, mk);
-        merge_owned<N2, VX>(wm, mk);
       }
       if (NI > DPM_IMG_X2P) {
         const uint32_t base = rp + 4 * (G::XP + lane + (16 / VX) * w);
-        add_owned<G::SOB, VX>(base, wp);
-        add_halo<G::SOB, VX, N2>(base, wp, lane);
+        add_window<G::SOB, VX, N2>(base, wp);
       }
       if (NI > DPM_IMG_X2M) {
         const uint32_t base = rp + 4 * (G::XM + lane + (16 / VX) * (NW - 1 - w));
-        add_owned<G::SOB, VX>(base, wm);
-        add_halo<G::SOB, VX, N2>(base, wm, lane);
+        add_window<G::SOB, VX, N2>(base, wm);
       }
     }
     }  // g.zc > 0
