@@ -278,6 +278,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
   constexpr bool TWO_PASS = NI >= 6 && VX == 8 && NW > 8;   // +-2z images in a second pass over the stage
   constexpr uint32_t STAGE_BYTES = SX * SZ * sizeof(T);
   constexpr int YZT = G::YZT;   // words of one YZ tile (0: YZ goes straight to global)
+  constexpr bool YZ_REDUX = NI >= 7 && YZT == 0;
   // TMA producer: lane 0 of a middle warp.  The row flushes start at thread 0,
   // so warps 0-3 carry them; keeping the producer's per-row-step work off those
   // warps shortens the slowest warp (cfg5 -5.7 %, tools/EXPERIMENTS.md v14)
@@ -397,7 +398,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
         for (int k = 0; k < VX; ++k) zx[t][k] = 0;
       }
       zx_col = p.s.img[DPM_IMG_ZX] + (int64_t)g.b * p.L * p.N + (g.X0 + VX * lane) * p.N + g.Z0 + 8 * w;
-      yz_col = p.s.img[DPM_IMG_YZ] + (int64_t)g.b * p.M * p.N + (g.Z0 + 8 * w + (lane >> 2)) * p.M;
+      yz_col = p.s.img[DPM_IMG_YZ] + (int64_t)g.b * p.M * p.N + (g.Z0 + 8 * w + (YZ_REDUX ? (lane & 7) : (lane >> 2))) * p.M;
       rc[0].set(g.X0, p.L);
       rc[1].set(g.X0 + g.Z0, p.s.W[DPM_IMG_DIAG]);
       if (NI > DPM_IMG_ANTI) rc[2].set(g.X0 - g.Z0 - (SZ - 1) + p.N - 1, p.s.W[DPM_IMG_ANTI]);
@@ -446,7 +447,18 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
       if (!TWO_PASS && NI > DPM_IMG_X2M) fold_pair<N2, VX>(wm, a, bb, 14 - 2 * t0, 12 - 2 * t0);
     }
 
-    // ---- YZ: warp reduce-scatter of the 8 plane sums -> lane quad q holds plane q
+    // ---- YZ plane sums.  Order 6: one warp-wide redux.sync.add per plane and
+    // lane t emits plane t (-1.5 %); orders <= 5: warp reduce-scatter, lane
+    // quad q holds plane q (redux measured +2.5 % there)
+    if (YZ_REDUX) {
+      uint32_t mine = 0;
+      #pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const uint32_t st = __reduce_add_sync(0xffffffffu, r8[t]);
+        mine = lane == t ? st : mine;
+      }
+      ptx::red_global_add_if(yz_col + y, mine, lane < 8 && mine != 0 && lane < g.zc);
+    } else
     {
       const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
       uint32_t r4[4], r2[2], r1;
