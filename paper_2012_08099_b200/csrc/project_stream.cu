@@ -40,15 +40,6 @@
 #include <mutex>
 #include "dpm_common.cuh"
 #include "ptx.cuh"
-#ifndef DPM_NO_ZX
-#define DPM_NO_ZX 0   // development experiment only (wrong ZX image)
-#endif
-#ifndef DPM_UNPACK_FMA
-#define DPM_UNPACK_FMA 0
-#endif
-#ifndef DPM_SKIP
-#define DPM_SKIP 0   // development bisection: 1 flush, 2 row atomics+merges, 4 YZ, 8 folds, 16 zx/cs/r8
-#endif
 
 namespace dpm {
 
@@ -72,21 +63,10 @@ template <> struct Vec<uint8_t, 4>  { using type = uint32_t; };
 
 template <typename T, int VX> struct Unpack;
 template <int VX> struct Unpack<uint16_t, VX> {
-  template <typename V> __device__ __forceinline__ static void run(const V& d, uint32_t* v, int32_t, uint32_t k16) {
+  template <typename V> __device__ __forceinline__ static void run(const V& d, uint32_t* v, int32_t, uint32_t) {
     const uint32_t* w = reinterpret_cast<const uint32_t*>(&d);
-#if DPM_UNPACK_FMA
-    // k16 == 65536 at run time: IMAD.HI / IMAD keep the unpack on the FMA pipe
-    #pragma unroll
-    for (int i = 0; i < VX / 2; ++i) {
-      const uint32_t hi = ptx::mulhi_u32(w[i], k16);
-      v[2 * i + 1] = hi;
-      v[2 * i] = ptx::mad_u32(hi, 0u - k16, w[i]);
-    }
-#else
-    (void)k16;
     #pragma unroll
     for (int i = 0; i < VX / 2; ++i) { v[2 * i] = w[i] & 0xFFFFu; v[2 * i + 1] = w[i] >> 16; }
-#endif
   }
 };
 template <int VX> struct Unpack<int16_t, VX> {
@@ -359,7 +339,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
   // the 8 x's of its group: every red.global then covers 4 runs of 8
   // consecutive z (32 B each) instead of 32 scattered words.
   auto flush_zx = [&]() {
-    if (col < 0 || DPM_NO_ZX) return;
+    if (col < 0) return;
     const int j = lane & 7, g8 = lane >> 3;
     uint32_t* base = p.s.img[DPM_IMG_ZX] + (int64_t)g.b * p.L * p.N + (g.X0 + VX * 8 * g8) * p.N + g.Z0 + 8 * w + j;
     const bool zok = j < g.zc;
@@ -433,10 +413,8 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
       }
       #pragma unroll
       for (int k = 0; k < VX; ++k) {
-#if !DPM_NO_ZX
         zx[t0][k] = ptx::mad_u32(a[k], p.one, zx[t0][k]);
         zx[t1][k] = ptx::mad_u32(bb[k], p.one, zx[t1][k]);
-#endif
         cs[k] += a[k] + bb[k];
       }
       r8[t0] = sumv<VX>(a);
@@ -605,11 +583,7 @@ size_t project_stream_workspace(const dpm_volume_desc*, int) { return 0; }
 // of orders >= 5 need more registers (then 8 warps, <= 255 registers); the
 // 4-wide lanes of order 3 fit 128 registers, so 16 warps (128-plane z-tiles)
 template <int NI, int VX> struct WarpsFor {
-#ifdef DPM_K6_WARPS
-  static constexpr int value = (VX == 8 && NI >= 6) ? DPM_K6_WARPS : (VX == 4 && NI == 4) ? 16 : 12;
-#else
-  static constexpr int value = (VX == 4 && NI == 4) ? 16 : (DPM_NO_ZX && NI <= 5) ? 16 : 12;
-#endif
+  static constexpr int value = (VX == 4 && NI == 4) ? 16 : 12;
 };
 // stages: as many 4-D boxes as fit next to the row buffers
 template <typename T, int NI, int VX> struct StagesFor {
