@@ -254,24 +254,23 @@ def main():
     ev_p1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     launches = [0]
 
-    graphed = None
+    graphed = stages = None
     if cfg != 5:
         graphed = engine.GraphedMoments(vox, order, offset=offset)   # captured once, replayed per step
+    else:
+        stages = engine.GraphedSlabStages(vox, order, offset=offset, z0=z0)   # three graphs; all-reduce between
 
     def step(i=None):
         if cfg == 5:
-            n_img = engine.num_images(order)
             if i is not None:
                 ev_p0[i].record(stream)
-            imgs = engine.project(vox, n_img, offset, z0)
-            lc = nat.last_launch_count()
+            stages.replay_project()
             if i is not None:
                 ev_p1[i].record(stream)
-            acc = engine.moments2d_images(vox, imgs, order, offset, z0)
-            lc += nat.last_launch_count()
-            pdist.allreduce_limbs(acc)
-            res = engine.derive(acc, order)
-            launches[0] += lc + res.launches
+            acc = stages.replay_moments2d()
+            pdist.allreduce_limbs(acc)           # the z-slab exchange (no-op at N=1)
+            res = stages.replay_derive()
+            launches[0] += stages.launches
             return res
         if i is not None:
             ev_p0[i].record(stream)

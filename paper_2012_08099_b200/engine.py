@@ -110,16 +110,19 @@ def image_layout(desc: nat.VolumeDesc, img: int) -> tuple[int, int, int, int]:
 
 
 def project(vox: torch.Tensor, n_img: int, offset: int = 0, z0: int = 0,
-            stream: torch.cuda.Stream | None = None) -> list[torch.Tensor]:
-    """Projection images 0..n_img-1 as int32 tensors [B, H, W] holding uint32 bits."""
+            stream: torch.cuda.Stream | None = None, imgs: list[torch.Tensor] | None = None,
+            workspace: torch.Tensor | None = None) -> list[torch.Tensor]:
+    """Projection images 0..n_img-1 as int32 tensors [B, H, W] holding uint32
+    bits (into ``imgs`` when given, e.g. for CUDA-graph capture)."""
     desc = make_desc(vox, offset, z0)
-    imgs = []
-    for k in range(n_img):
-        W, H, _, _ = image_layout(desc, k)
-        imgs.append(torch.empty((desc.B, H, W), dtype=torch.int32, device=vox.device))
+    if imgs is None:
+        imgs = []
+        for k in range(n_img):
+            W, H, _, _ = image_layout(desc, k)
+            imgs.append(torch.empty((desc.B, H, W), dtype=torch.int32, device=vox.device))
     ptrs = (ctypes.c_void_p * n_img)(*[t.data_ptr() for t in imgs])
     wsb = int(nat.lib().dpm_project_workspace_bytes(ctypes.byref(desc), n_img))
-    ws = _WS.get(wsb, vox.device) if wsb else None
+    ws = (workspace if workspace is not None else _WS.get(wsb, vox.device)) if wsb else None
     nat.check(nat.lib().dpm_project(ctypes.byref(desc), vox.data_ptr(), n_img, ptrs,
                                     ws.data_ptr() if ws is not None else None, wsb, stream_handle(stream)),
               "dpm_project")
@@ -170,13 +173,14 @@ def moments(vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0, n_globa
 
 
 def moments2d_images(vox: torch.Tensor, imgs: list[torch.Tensor], order: int, offset: int = 0, z0: int = 0,
-                     stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+                     stream: torch.cuda.Stream | None = None, acc: torch.Tensor | None = None) -> torch.Tensor:
     """Exact 2D moments (global coordinates) of images made by ``project`` from
     ``vox``; returns the limb accumulator [B, n_img, n2d, 4] (int64 storage of
-    uint64 sums)."""
+    uint64 sums), written into ``acc`` when given."""
     desc = make_desc(vox, offset, z0)
     n_img = len(imgs)
-    acc = torch.empty((desc.B, n_img, n2d(order), 4), dtype=torch.int64, device=vox.device)
+    if acc is None:
+        acc = torch.empty((desc.B, n_img, n2d(order), 4), dtype=torch.int64, device=vox.device)
     ptrs = (ctypes.c_void_p * n_img)(*[t.data_ptr() for t in imgs])
     nat.check(nat.lib().dpm_moments2d(ctypes.byref(desc), n_img, ptrs, order, acc.data_ptr(),
                                       stream_handle(stream)), "dpm_moments2d")
@@ -193,7 +197,8 @@ def moments2d_partial(vox: torch.Tensor, order: int, offset: int = 0, z0: int = 
     return moments2d_images(vox, imgs, order, offset, z0, stream)
 
 
-def derive(acc: torch.Tensor, order: int, stream: torch.cuda.Stream | None = None) -> DeviceMoments:
+def derive(acc: torch.Tensor, order: int, stream: torch.cuda.Stream | None = None,
+           out: DeviceMoments | None = None) -> DeviceMoments:
     """Device epilogue on a (possibly summed) limb accumulator."""
     check_order(order)
     B = acc.shape[0]
@@ -201,10 +206,11 @@ def derive(acc: torch.Tensor, order: int, stream: torch.cuda.Stream | None = Non
     desc.L = desc.M = desc.N = 1
     desc.B = B
     dev = acc.device
-    out = DeviceMoments(
-        i128=torch.empty((B, n3d(order), 2), dtype=torch.int64, device=dev),
-        f64=torch.empty((B, n3d(order)), dtype=torch.float64, device=dev),
-        status=torch.empty((B,), dtype=torch.int32, device=dev), launches=0)
+    if out is None:
+        out = DeviceMoments(
+            i128=torch.empty((B, n3d(order), 2), dtype=torch.int64, device=dev),
+            f64=torch.empty((B, n3d(order)), dtype=torch.float64, device=dev),
+            status=torch.empty((B,), dtype=torch.int32, device=dev), launches=0)
     nat.check(nat.lib().dpm_derive3d(ctypes.byref(desc), acc.data_ptr(), order, out.i128.data_ptr(),
                                      out.f64.data_ptr(), out.status.data_ptr(), stream_handle(stream)),
               "dpm_derive3d")
@@ -282,6 +288,66 @@ class GraphedMoments:
 
     def replay(self) -> DeviceMoments:
         self.graph.replay()
+        return self.out
+
+
+class GraphedSlabStages:
+    """The z-slab pipeline as three CUDA graphs over fixed buffers: (1) the
+    projection (image zeroing + streaming pass), (2) exact 2D moments in
+    global coordinates into ``acc``, (3) the epilogue into ``out``.  A
+    multi-GPU caller all-reduces ``acc`` between (2) and (3) (the exchange is
+    not captured).  Replays are issued on the caller's current stream."""
+
+    def __init__(self, vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0):
+        check_order(order)
+        self.vox, self.order, self.offset, self.z0 = vox, order, offset, z0
+        desc = make_desc(vox, offset, z0)
+        n_img = num_images(order)
+        dev = vox.device
+        self.imgs = []
+        for k in range(n_img):
+            W, H, _, _ = image_layout(desc, k)
+            self.imgs.append(torch.empty((desc.B, H, W), dtype=torch.int32, device=dev))
+        wsb = int(nat.lib().dpm_project_workspace_bytes(ctypes.byref(desc), n_img))
+        self.ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device=dev) if wsb else None
+        self.acc = torch.empty((desc.B, n_img, n2d(order), 4), dtype=torch.int64, device=dev)
+        self.out = DeviceMoments(
+            i128=torch.empty((desc.B, n3d(order), 2), dtype=torch.int64, device=dev),
+            f64=torch.empty((desc.B, n3d(order)), dtype=torch.float64, device=dev),
+            status=torch.empty((desc.B,), dtype=torch.int32, device=dev), launches=0)
+        stages = [self._project, self._moments2d, self._derive]
+        st = torch.cuda.Stream(device=dev)
+        st.wait_stream(torch.cuda.current_stream(dev))
+        self.graphs, self.launches = [], 0
+        with torch.cuda.stream(st):
+            for fn in stages:                  # warm-up: attributes, tensor-map encoder
+                fn()
+                self.launches += nat.last_launch_count()
+            for fn in stages:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=st):
+                    fn()
+                self.graphs.append(g)
+        torch.cuda.current_stream(dev).wait_stream(st)
+
+    def _project(self):
+        project(self.vox, len(self.imgs), self.offset, self.z0, imgs=self.imgs, workspace=self.ws)
+
+    def _moments2d(self):
+        moments2d_images(self.vox, self.imgs, self.order, self.offset, self.z0, acc=self.acc)
+
+    def _derive(self):
+        derive(self.acc, self.order, out=self.out)
+
+    def replay_project(self) -> None:
+        self.graphs[0].replay()
+
+    def replay_moments2d(self) -> torch.Tensor:
+        self.graphs[1].replay()
+        return self.acc
+
+    def replay_derive(self) -> DeviceMoments:
+        self.graphs[2].replay()
         return self.out
 
 

@@ -95,3 +95,23 @@ def test_strided_views(cuda, case):
     want_imgs = oracle.project(np.ascontiguousarray(vols[0]), 7)
     for k in range(7):
         assert np.array_equal(imgs[k][0].cpu().numpy().view(np.uint32), want_imgs[k].astype(np.uint32)), k
+
+
+@pytest.mark.parametrize("order", [4, 6])
+def test_graphed_slab_stages(cuda, order):
+    """Three-graph z-slab pipeline (projection, 2D moments, epilogue) == the
+    eager path, replay after replay, on a slab in global coordinates."""
+    rng = np.random.default_rng(order)
+    full = rng.integers(0, 65535, size=(40, 24, 264)).astype(np.uint16)
+    z0, n = 16, 24
+    slab = torch.from_numpy(full[z0:z0 + n]).cuda()
+    st = engine.GraphedSlabStages(slab, order, z0=z0)
+    want_acc = engine.moments2d_partial(slab, order, z0=z0)
+    for _ in range(2):
+        st.replay_project()
+        acc = st.replay_moments2d()
+        assert torch.equal(acc, want_acc)
+        res = st.replay_derive()
+        torch.cuda.synchronize()
+        assert torch.equal(res.i128, engine.derive(want_acc, order).i128)
+    assert st.launches == 3
