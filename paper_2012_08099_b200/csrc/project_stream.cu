@@ -160,6 +160,14 @@ struct Cursor {
     if (++yoff == yb) { yoff = 0; ++c; }
   }
   __device__ __forceinline__ int32_t y() const { return y0 + yoff; }
+  // rows left in the current column within this band and this CTA's run
+  __device__ __forceinline__ int32_t run() const { return left < yb - yoff ? left : yb - yoff; }
+  __device__ __forceinline__ void advance_by(const StreamParams& p, int32_t n) {
+    left -= n;
+    if (left == 0) { y0 += (int32_t)p.band; band_setup(p); return; }
+    yoff += n;
+    if (yoff == yb) { yoff = 0; ++c; }
+  }
 };
 
 
@@ -367,7 +375,6 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
   };
 
   while (!cur.done) {
-    const int32_t y = cur.y();
     if (cur.c != col) {
       flush_zx();
       col = cur.c;
@@ -385,6 +392,9 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
       if (NI > DPM_IMG_X2P) rc[3].set(g.X0 + 2 * g.Z0, p.s.W[DPM_IMG_X2P]);
       if (NI > DPM_IMG_X2M) rc[4].set(g.X0 - 2 * g.Z0 - 2 * (SZ - 1) + 2 * (p.N - 1), p.s.W[DPM_IMG_X2M]);
     }
+    // consecutive rows of this column: no column or band logic per row-step
+    const int32_t y_first = cur.y(), y_end = y_first + cur.run();
+    for (int32_t y = y_first; y < y_end; ++y) {
     if (g.zc > 0) {   // warp-uniform: warps past the volume's last plane only join the barrier
     ptx::mbar_wait_addr(full_addr + 8u * cst, cphase);
     const T* tile = reinterpret_cast<const T*>(stages + cst * STAGE_BYTES) + (8 * w) * SX + VX * lane;
@@ -527,10 +537,9 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     }
     parity ^= 1;
     if (++cst == STAGES) { cst = 0; cphase ^= 1u; }
-    cur.advance(p);
-    // YZ tile -> image once 8 consecutive y are in (or the run of y breaks):
+    // YZ tile -> image once 8 consecutive y are in (or the run of y ends):
     // 8 threads cover 32 contiguous bytes of a z-row
-    if (YZT > 0 && (cur.done || cur.c != col || cur.y() != y + 1 || ((y + 1) & 7) == 0)) {
+    if (YZT > 0 && (y + 1 == y_end || ((y + 1) & 7) == 0)) {
       uint32_t* tb = yzb + yzpar * SZ * 8;
       uint32_t* gy = p.s.img[DPM_IMG_YZ] + (int64_t)g.b * p.M * p.N + g.Z0 * p.M + (y & ~7);
       const int ty = tid;   // (spreading the flushes over all warps measured slower: 4 %)
@@ -544,6 +553,8 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
       }
       yzpar ^= 1;
     }
+    }  // rows of the run
+    cur.advance_by(p, y_end - y_first);
   }
   flush_zx();
 }
