@@ -522,17 +522,20 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     // ---- flush this row-step's CTA rows -------------------------------------
     {
       uint32_t* rw = rows + parity * G::WORDS;
-      const int64_t rowid = (int64_t)g.b * p.M + y;
-      flush_region<VX, G::SXY, SX, THREADS>(rw + G::XY, tid, p.s.img[DPM_IMG_XY] + rowid * p.L + rc[0].g0, rc[0].lo, rc[0].hi);
-      const int64_t Wd = p.s.W[DPM_IMG_DIAG];
-      flush_region<VX, G::SOB, G::W1, THREADS>(rw + G::DG, tid, p.s.img[DPM_IMG_DIAG] + rowid * Wd + rc[1].g0, rc[1].lo, rc[1].hi);
+      // 32-bit row index and widths (the host checks B*M and W < 2^31 for this
+      // kernel): one IMAD.WIDE.U32 per region instead of 64-bit multiplies
+      const uint32_t rowid = (uint32_t)g.b * (uint32_t)p.M + (uint32_t)y;
+      auto row = [&](int k, uint32_t w32, int64_t g0) { return p.s.img[k] + ((uint64_t)rowid * w32 + g0); };
+      flush_region<VX, G::SXY, SX, THREADS>(rw + G::XY, tid, row(DPM_IMG_XY, (uint32_t)p.L, rc[0].g0), rc[0].lo, rc[0].hi);
+      const uint32_t Wd = (uint32_t)p.s.W[DPM_IMG_DIAG];
+      flush_region<VX, G::SOB, G::W1, THREADS>(rw + G::DG, tid, row(DPM_IMG_DIAG, Wd, rc[1].g0), rc[1].lo, rc[1].hi);
       if (NI > DPM_IMG_ANTI)
-        flush_region<VX, G::SOB, G::W1, THREADS>(rw + G::AN, tid, p.s.img[DPM_IMG_ANTI] + rowid * Wd + rc[2].g0, rc[2].lo, rc[2].hi);
+        flush_region<VX, G::SOB, G::W1, THREADS>(rw + G::AN, tid, row(DPM_IMG_ANTI, Wd, rc[2].g0), rc[2].lo, rc[2].hi);
       if (NI > DPM_IMG_X2P) {
-        const int64_t W2g = p.s.W[DPM_IMG_X2P];
-        flush_region<VX, G::SOB, G::W2, THREADS>(rw + G::XP, tid, p.s.img[DPM_IMG_X2P] + rowid * W2g + rc[3].g0, rc[3].lo, rc[3].hi);
+        const uint32_t W2g = (uint32_t)p.s.W[DPM_IMG_X2P];
+        flush_region<VX, G::SOB, G::W2, THREADS>(rw + G::XP, tid, row(DPM_IMG_X2P, W2g, rc[3].g0), rc[3].lo, rc[3].hi);
         if (NI > DPM_IMG_X2M)
-          flush_region<VX, G::SOB, G::W2, THREADS>(rw + G::XM, tid, p.s.img[DPM_IMG_X2M] + rowid * W2g + rc[4].g0, rc[4].lo, rc[4].hi);
+          flush_region<VX, G::SOB, G::W2, THREADS>(rw + G::XM, tid, row(DPM_IMG_X2M, W2g, rc[4].g0), rc[4].lo, rc[4].hi);
       }
     }
     parity ^= 1;
@@ -585,6 +588,7 @@ static bool stream_eligible(const dpm_volume_desc* d, const void* vox) {
   if (d->L % lane_width(d)) return false;  // a lane vector never straddles the row end
   if (reinterpret_cast<uintptr_t>(vox) % 16) return false;
   if (d->L > 0x7fffffffLL || d->M > 0x7fffffffLL || d->N > 0x7fffffffLL || d->B > 0x7fffffffLL) return false;
+  if (d->B * d->M > 0x7fffffffLL || d->L + 2 * d->N > 0x7fffffffLL) return false;   // 32-bit row ids / widths
   return encode_fn() != nullptr;
 }
 
