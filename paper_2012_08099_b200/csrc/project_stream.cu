@@ -409,10 +409,14 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     for (int i = 0; i < N2; ++i) { wp[i] = 0; wm[i] = 0; }
     V dv[8];
     #pragma unroll
-    for (int t = 0; t < 8; ++t) dv[t] = *reinterpret_cast<const V*>(tile + t * SX);   // issue all loads first
+    for (int t = 0; t < 4; ++t) dv[t] = *reinterpret_cast<const V*>(tile + t * SX);
     #pragma unroll
     for (int tp = 0; tp < 4; ++tp) {
       const int t0 = 2 * tp, t1 = t0 + 1;
+      if (tp >= 1 && tp <= 2) {   // two plane pairs in flight (16 fewer live registers than all 8 up front)
+        #pragma unroll
+        for (int t = 2 * tp + 2; t < 2 * tp + 4; ++t) dv[t] = *reinterpret_cast<const V*>(tile + t * SX);
+      }
       uint32_t a[VX], bb[VX];
       Unpack<T, VX>::run(dv[t0], a, p.offset, p.one << 16);
       Unpack<T, VX>::run(dv[t1], bb, p.offset, p.one << 16);
