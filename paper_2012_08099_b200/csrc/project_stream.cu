@@ -400,6 +400,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     const T* tile = reinterpret_cast<const T*>(stages + cst * STAGE_BYTES) + (8 * w) * SX + VX * lane;
 
     uint32_t cs[VX], r8[8];
+    uint32_t yzmine = 0;   // order 6: plane (lane) sum, reduced as soon as each plane is folded
     uint32_t wd[N1], wa[N1], wp[N2], wm[N2];
     #pragma unroll
     for (int i = 0; i < VX; ++i) cs[i] = 0;
@@ -431,8 +432,14 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
         zx[t1][k] = ptx::mad_u32(bb[k], p.one, zx[t1][k]);
         cs[k] += a[k] + bb[k];
       }
-      r8[t0] = sumv<VX>(a);
-      r8[t1] = sumv<VX>(bb);
+      if (YZ_REDUX) {
+        const uint32_t s0 = __reduce_add_sync(0xffffffffu, sumv<VX>(a));
+        const uint32_t s1 = __reduce_add_sync(0xffffffffu, sumv<VX>(bb));
+        yzmine = lane == t0 ? s0 : (lane == t1 ? s1 : yzmine);
+      } else {
+        r8[t0] = sumv<VX>(a);
+        r8[t1] = sumv<VX>(bb);
+      }
       fold_pair<N1, VX>(wd, a, bb, t0, t0 + 1);
       if (NI > DPM_IMG_ANTI) fold_pair<N1, VX>(wa, a, bb, 7 - t0, 6 - t0);
       if (!TWO_PASS && NI > DPM_IMG_X2P) fold_pair<N2, VX>(wp, a, bb, 2 * t0, 2 * t0 + 2);
@@ -443,13 +450,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     // lane t emits plane t (-1.5 %); orders <= 5: warp reduce-scatter, lane
     // quad q holds plane q (redux measured +2.5 % there)
     if (YZ_REDUX) {
-      uint32_t mine = 0;
-      #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const uint32_t st = __reduce_add_sync(0xffffffffu, r8[t]);
-        mine = lane == t ? st : mine;
-      }
-      ptx::red_global_add_if(yz_col + y, mine, lane < 8 && mine != 0 && lane < g.zc);
+      ptx::red_global_add_if(yz_col + y, yzmine, lane < 8 && yzmine != 0 && lane < g.zc);
     } else
     {
       const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
