@@ -337,7 +337,11 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
   g.X0 = g.Z0 = 0; g.b = 0; g.zc = 0; g.xok = false;
   uint32_t* zx_col = nullptr;
   uint32_t* yz_col = nullptr;
-  RegionCol rc[5];
+  // flush geometry of the current column: identical for all threads, so it
+  // lives in shared memory (two slots by column parity: thread 0 fills the
+  // next column's slot while others may still flush the previous column)
+  RegionCol* rcs = reinterpret_cast<RegionCol*>(reinterpret_cast<uint8_t*>(full + STAGES) + 64);
+  int rslot = 0;
   int cst = 0, parity = 0, yzpar = 0;
   uint32_t cphase = 0;
 
@@ -386,11 +390,15 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
       }
       zx_col = p.s.img[DPM_IMG_ZX] + (int64_t)g.b * p.L * p.N + (g.X0 + VX * lane) * p.N + g.Z0 + 8 * w;
       yz_col = p.s.img[DPM_IMG_YZ] + (int64_t)g.b * p.M * p.N + (g.Z0 + 8 * w + (YZ_REDUX ? (lane & 7) : (lane >> 2))) * p.M;
-      rc[0].set(g.X0, p.L);
-      rc[1].set(g.X0 + g.Z0, p.s.W[DPM_IMG_DIAG]);
-      if (NI > DPM_IMG_ANTI) rc[2].set(g.X0 - g.Z0 - (SZ - 1) + p.N - 1, p.s.W[DPM_IMG_ANTI]);
-      if (NI > DPM_IMG_X2P) rc[3].set(g.X0 + 2 * g.Z0, p.s.W[DPM_IMG_X2P]);
-      if (NI > DPM_IMG_X2M) rc[4].set(g.X0 - 2 * g.Z0 - 2 * (SZ - 1) + 2 * (p.N - 1), p.s.W[DPM_IMG_X2M]);
+      rslot ^= 1;
+      if (tid == 0) {
+        RegionCol* rc = rcs + 5 * rslot;
+        rc[0].set(g.X0, p.L);
+        rc[1].set(g.X0 + g.Z0, p.s.W[DPM_IMG_DIAG]);
+        if (NI > DPM_IMG_ANTI) rc[2].set(g.X0 - g.Z0 - (SZ - 1) + p.N - 1, p.s.W[DPM_IMG_ANTI]);
+        if (NI > DPM_IMG_X2P) rc[3].set(g.X0 + 2 * g.Z0, p.s.W[DPM_IMG_X2P]);
+        if (NI > DPM_IMG_X2M) rc[4].set(g.X0 - 2 * g.Z0 - 2 * (SZ - 1) + 2 * (p.N - 1), p.s.W[DPM_IMG_X2M]);
+      }
     }
     // consecutive rows of this column: no column or band logic per row-step
     const int32_t y_first = cur.y(), y_end = y_first + cur.run();
@@ -531,6 +539,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
       // kernel): one IMAD.WIDE.U32 per region instead of 64-bit multiplies
       const uint32_t rowid = (uint32_t)g.b * (uint32_t)p.M + (uint32_t)y;
       auto row = [&](int k, uint32_t w32, int64_t g0) { return p.s.img[k] + ((uint64_t)rowid * w32 + g0); };
+      const RegionCol* rc = rcs + 5 * rslot;   // written before this column's first barrier
       flush_region<VX, G::SXY, SX, THREADS>(rw + G::XY, tid, row(DPM_IMG_XY, (uint32_t)p.L, rc[0].g0), rc[0].lo, rc[0].hi);
       const uint32_t Wd = (uint32_t)p.s.W[DPM_IMG_DIAG];
       flush_region<VX, G::SOB, G::W1, THREADS>(rw + G::DG, tid, row(DPM_IMG_DIAG, Wd, rc[1].g0), rc[1].lo, rc[1].hi);
@@ -619,7 +628,7 @@ static int launch_one(const dpm_volume_desc* d, const void* vox, int grid, cudaS
   constexpr int NW = WarpsFor<NI, VX>::value;
   constexpr int S = StagesFor<T, NI, VX>::value;
   using G = Geo<NI, NW, VX>;
-  constexpr size_t bytes = (size_t)S * G::SX * G::SZ * sizeof(T) + 2 * G::WORDS * 4 + 2 * G::YZT * 4 + S * 8 + 64;
+  constexpr size_t bytes = (size_t)S * G::SX * G::SZ * sizeof(T) + 2 * G::WORDS * 4 + 2 * G::YZT * 4 + S * 8 + 64 + 160;
   static_assert(bytes <= 227 * 1024, "shared memory budget");
   const int64_t es = sizeof(T);
   CUtensorMap map;
