@@ -30,7 +30,8 @@
 //             __syncthreads per row-step the row is flushed to global memory
 //             (coalesced predicated red.global of non-zero cells) and re-zeroed;
 //             rows are double-buffered.
-//   YZ (y,z)  per-plane lane sums, warp reduce-scatter, one red.global per (z,y).
+//   YZ (y,z)  per-plane lane sums, one warp redux per plane, one red.global per (z,y)
+//             (orders <= 5: staged per 8 consecutive y in shared memory).
 // Work split: row-steps are grouped into y-bands sized so a band's image rows
 // stay L2-resident; within a band the (column, y) sequence is cut into equal
 // contiguous runs, one per persistent CTA.
@@ -266,7 +267,6 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
   constexpr bool TWO_PASS = NI >= 6 && VX == 8 && NW > 8;   // +-2z images in a second pass over the stage
   constexpr uint32_t STAGE_BYTES = SX * SZ * sizeof(T);
   constexpr int YZT = G::YZT;   // words of one YZ tile (0: YZ goes straight to global)
-  constexpr bool YZ_REDUX = NI >= 7 && YZT == 0;
   // TMA producer: lane 0 of a middle warp.  The row flushes start at thread 0,
   // so warps 0-3 carry them; keeping the producer's per-row-step work off those
   // warps shortens the slowest warp (cfg5 -5.7 %, tools/EXPERIMENTS.md v14)
@@ -389,7 +389,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
         for (int k = 0; k < VX; ++k) zx[t][k] = 0;
       }
       zx_col = p.s.img[DPM_IMG_ZX] + (int64_t)g.b * p.L * p.N + (g.X0 + VX * lane) * p.N + g.Z0 + 8 * w;
-      yz_col = p.s.img[DPM_IMG_YZ] + (int64_t)g.b * p.M * p.N + (g.Z0 + 8 * w + (YZ_REDUX ? (lane & 7) : (lane >> 2))) * p.M;
+      yz_col = p.s.img[DPM_IMG_YZ] + (int64_t)g.b * p.M * p.N + (g.Z0 + 8 * w + (lane & 7)) * p.M;
       rslot ^= 1;
       if (tid == 0) {
         RegionCol* rc = rcs + 5 * rslot;
@@ -407,8 +407,8 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     ptx::mbar_wait_addr(full_addr + 8u * cst, cphase);
     const T* tile = reinterpret_cast<const T*>(stages + cst * STAGE_BYTES) + (8 * w) * SX + VX * lane;
 
-    uint32_t cs[VX], r8[8];
-    uint32_t yzmine = 0;   // order 6: plane (lane) sum, reduced as soon as each plane is folded
+    uint32_t cs[VX];
+    uint32_t yzmine = 0;   // lane t < 8: this warp's plane t sum (YZ), reduced as each plane pair is folded
     uint32_t wd[N1], wa[N1], wp[N2], wm[N2];
     #pragma unroll
     for (int i = 0; i < VX; ++i) cs[i] = 0;
@@ -440,13 +440,10 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
         zx[t1][k] = ptx::mad_u32(bb[k], p.one, zx[t1][k]);
         cs[k] += a[k] + bb[k];
       }
-      if (YZ_REDUX) {
+      {   // YZ: warp-wide redux of the plane sums (one REDUX per plane)
         const uint32_t s0 = __reduce_add_sync(0xffffffffu, sumv<VX>(a));
         const uint32_t s1 = __reduce_add_sync(0xffffffffu, sumv<VX>(bb));
         yzmine = lane == t0 ? s0 : (lane == t1 ? s1 : yzmine);
-      } else {
-        r8[t0] = sumv<VX>(a);
-        r8[t1] = sumv<VX>(bb);
       }
       fold_pair<N1, VX>(wd, a, bb, t0, t0 + 1);
       if (NI > DPM_IMG_ANTI) fold_pair<N1, VX>(wa, a, bb, 7 - t0, 6 - t0);
@@ -454,39 +451,14 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
       if (!TWO_PASS && NI > DPM_IMG_X2M) fold_pair<N2, VX>(wm, a, bb, 14 - 2 * t0, 12 - 2 * t0);
     }
 
-    // ---- YZ plane sums.  Order 6: one warp-wide redux.sync.add per plane and
-    // lane t emits plane t (-1.5 %); orders <= 5: warp reduce-scatter, lane
-    // quad q holds plane q (redux measured +2.5 % there)
-    if (YZ_REDUX) {
+    // ---- YZ: lane t < 8 holds plane t of this warp (reduced in the fold loop)
+    if (YZT > 0) {
+      if (lane < 8) yzb[yzpar * SZ * 8 + (8 * w + lane) * 8 + (y & 7)] = yzmine;
+    } else {
       ptx::red_global_add_if(yz_col + y, yzmine, lane < 8 && yzmine != 0 && lane < g.zc);
-    } else
-    {
-      const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
-      uint32_t r4[4], r2[2], r1;
-      #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t send = h16 ? r8[j] : r8[j + 4], keep = h16 ? r8[j + 4] : r8[j];
-        r4[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-      }
-      #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const uint32_t send = h8 ? r4[j] : r4[j + 2], keep = h8 ? r4[j + 2] : r4[j];
-        r2[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-      }
-      {
-        const uint32_t send = h4 ? r2[0] : r2[1], keep = h4 ? r2[1] : r2[0];
-        r1 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-      }
-      r1 += __shfl_xor_sync(0xffffffffu, r1, 2);
-      r1 += __shfl_xor_sync(0xffffffffu, r1, 1);
-      if (YZT > 0) {
-        if ((lane & 3) == 0) yzb[yzpar * SZ * 8 + (8 * w + (lane >> 2)) * 8 + (y & 7)] = r1;
-      } else {
-        ptx::red_global_add_if(yz_col + y, r1, (lane & 3) == 0 && r1 != 0 && (lane >> 2) < g.zc);
-      }
     }
 
-    // ---- merge window overlaps, add owned cells (and the tile's halo) into the CTA rows
+    // ---- add the XY column sums and the oblique windows to the CTA rows
     {
       const uint32_t rp = rows_addr + (uint32_t)(parity * G::WORDS * 4);
       add_owned<G::SXY, VX>(rp + 4 * (G::XY + lane), cs);
