@@ -14,27 +14,32 @@
 //              the image rows being reduced into).
 //   CTA      = NW warps, warp w owns planes Z0+8w..+7, lane l owns x = X0+VX*l..+VX-1:
 //              each lane reduces a VX (x) x 8 (z) patch per row-step (VX = 8, or
-//              4 for narrow volumes such as the 128^3 batch).  NW is
-//              the largest warp count whose register budget fits the order:
-//              12 (3 warps/SMSP, <= 168 regs) for K <= 4, 8 (<= 255 regs) above.
+//              4 for narrow volumes such as the 128^3 batch).  NW = 12 (3 warps
+//              per scheduler, <= 168 registers; 16 for 4-wide lanes at order 3);
+//              at order 6 the (x +- 2z) images are folded in a second pass over
+//              the same stage to stay within that budget.  The TMA producer is
+//              lane 0 of warp NW/2 (the row flush lands on warps 0-3).
 //   ZX (x,z)  sum over y: 8*VX registers per lane, persistent across the
-//             row-steps of a column (adds on the FMA pipe), flushed with
-//             red.global when the CTA's run leaves the column.
+//             row-steps of a column (adds on the FMA pipe), flushed at the end
+//             of the CTA's run through the column: an 8x8 shfl.xor transpose
+//             per 8-lane group makes every red.global cover 32-byte runs of z.
 //   XY and the oblique images (x + t z, y), t = 1, -1, 2, -2: plane pairs are
 //             folded into VX / VX+7 / VX+14-cell register windows with 3-input
-//             adds; window overlap with higher lanes moves by predicated
-//             shfl.up, and each lane red.shared's its VX owned cells into the
-//             CTA row, stored transposed (cell i at (i%VX)*S + i/VX,
-//             S = 32/VX mod 32) so those
-//             reductions and the flush reads are bank-conflict free.  After one
-//             __syncthreads per row-step the row is flushed to global memory
-//             (coalesced predicated red.global of non-zero cells) and re-zeroed;
-//             rows are double-buffered.
-//   YZ (y,z)  per-plane lane sums, one warp redux per plane, one red.global per (z,y)
-//             (orders <= 5: staged per 8 consecutive y in shared memory).
+//             adds, and every lane adds its WHOLE window to the CTA row with
+//             red.shared.  Rows are stored transposed (cell i at
+//             (i%VX)*S + i/VX, S = 32/VX mod 32), so window cell c of the 32
+//             lanes is 32 consecutive words: conflict-free, and the overlaps
+//             between neighbouring lanes (and the tile halo) are resolved by
+//             the atomics themselves.  After one __syncthreads per row-step the
+//             rows are flushed to global memory (LDS.128 + coalesced red.global)
+//             and re-zeroed; rows are double-buffered.
+//   YZ (y,z)  per-plane lane sums, one warp redux per plane inside the fold
+//             loop, one red.global per (z,y) (orders <= 5: staged per 8
+//             consecutive y in shared memory, flushed coalesced).
 // Work split: row-steps are grouped into y-bands sized so a band's image rows
 // stay L2-resident; within a band the (column, y) sequence is cut into equal
-// contiguous runs, one per persistent CTA.
+// contiguous runs, one per persistent CTA, iterated as runs of consecutive
+// rows of one column.
 // Exactness: uint32 ray sums (the C ABI rejects shapes whose longest ray could
 // reach 2^32) and associative integer atomics: bit-identical to the reference.
 #include <cudaTypedefs.h>
