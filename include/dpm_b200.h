@@ -106,6 +106,13 @@ DPM_API size_t dpm_project_workspace_bytes(const dpm_volume_desc* desc, int n_im
 DPM_API int dpm_project(const dpm_volume_desc* desc, const void* d_voxels, int n_img,
                 uint32_t* const* d_images, void* d_ws, size_t ws_bytes, void* stream);
 
+/* The same projection pass through the shape-generic brick kernel only (never
+ * the TMA streaming kernel): an independent second implementation, registered
+ * as the "dpm_generic" engine so verify_engines (harness.py:101-120) has two
+ * device engines to cross-check, as the reference cross-checks its three. */
+DPM_API int dpm_project_generic(const dpm_volume_desc* desc, const void* d_voxels, int n_img,
+                uint32_t* const* d_images, void* stream);
+
 /* Exact 2D raw moments M_pq = sum I[j][i] (i+ai)^p (j+aj)^q, p+q <= order, of
  * images laid out by `desc`.  Replaces drt2d.integrals + assemble_2d +
  * shift_origin (drt2d.py:92-208) and exact.weighted_power_sums (exact.py:63-82).

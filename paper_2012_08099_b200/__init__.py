@@ -6,18 +6,18 @@ moments, with every stage running in hand-written sm_100a CUDA kernels behind
 the C ABI in include/dpm_b200.h.  There is no CPU fallback: without the CUDA
 library (paper_2012_08099_b200/libdpm_b200.so) and a GPU, compute calls raise.
 """
-from . import drt2d
+from . import drt2d, harness
 from .counters import OpCounters
 from .drt2d import Moments2D, brute_force_2d, image_moments, shift_origin
 from .errors import FormatError, InconsistencyError
 from .features import (CentralMoments3, ShapeFeatures, apply_spacing, central_moments, centroid, feature_report,
                        normalize_scale, shape_features)
-from .moments3d import (ENGINES, MomentTensor3, count_ops, dpm_moments, dpm_moments_batch,
+from .moments3d import (ENGINES, MomentTensor3, count_ops, dpm_generic_moments, dpm_moments, dpm_moments_batch,
                         dpm_moments_file, moment_indices)
 from .projection import (ANGLES, Orientation, ProjectionImage, ProjectionSet, project, project_all,
                          project_extended, project_subset, write_pgm)
 from .volio import VolumeMeta, load_nrrd, load_raw, meta_from_header_file, open_nrrd, open_raw, write_raw
-from .volume import Volume, delta, ellipsoid, random, uniform
+from .volume import Volume, delta, ellipsoid, random, synth, uniform
 
 __version__ = "0.1.0"
 
@@ -25,7 +25,7 @@ __all__ = [
     "ANGLES", "CentralMoments3", "ENGINES", "FormatError", "ShapeFeatures", "apply_spacing", "central_moments",
     "centroid", "feature_report", "normalize_scale", "shape_features", "InconsistencyError", "Moments2D", "MomentTensor3", "OpCounters",
     "Orientation", "ProjectionImage", "ProjectionSet", "Volume", "count_ops", "delta",
-    "VolumeMeta", "brute_force_2d", "dpm_moments", "dpm_moments_batch", "dpm_moments_file", "drt2d",
+    "VolumeMeta", "brute_force_2d", "dpm_generic_moments", "dpm_moments", "dpm_moments_batch", "harness", "synth", "dpm_moments_file", "drt2d",
     "ellipsoid", "image_moments", "load_nrrd", "load_raw", "meta_from_header_file", "open_nrrd", "open_raw",
     "moment_indices", "project", "project_all",
     "project_extended", "project_subset", "random", "shift_origin", "uniform", "write_pgm", "write_raw",

@@ -26,6 +26,7 @@ EXPORTS = (
     "dpm_project_workspace_bytes", "dpm_project", "dpm_moments2d", "dpm_derive3d",
     "dpm_workspace_bytes", "dpm_moments", "dpm_check_envelope", "dpm_acc_add",
     "dpm_synth_noise_u16", "dpm_last_launch_count", "dpm_strerror", "dpm_image_moments2d",
+    "dpm_project_generic",
 )
 
 
@@ -62,6 +63,7 @@ def lib() -> ctypes.CDLL:
         "dpm_image_layout": (ctypes.c_int, [pdesc, ctypes.c_int] + [ctypes.POINTER(i64)] * 4),
         "dpm_project_workspace_bytes": (sz, [pdesc, ctypes.c_int]),
         "dpm_project": (ctypes.c_int, [pdesc, vp, ctypes.c_int, ctypes.POINTER(vp), vp, sz, vp]),
+        "dpm_project_generic": (ctypes.c_int, [pdesc, vp, ctypes.c_int, ctypes.POINTER(vp), vp]),
         "dpm_moments2d": (ctypes.c_int, [pdesc, ctypes.c_int, ctypes.POINTER(vp), ctypes.c_int, vp, vp]),
         "dpm_derive3d": (ctypes.c_int, [pdesc, vp, ctypes.c_int, vp, vp, vp, vp]),
         "dpm_image_moments2d": (ctypes.c_int, [vp, i64, i64, i64, i64, ctypes.c_int, vp, vp]),

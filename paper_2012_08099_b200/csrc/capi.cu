@@ -116,6 +116,22 @@ int dpm_project(const dpm_volume_desc* desc, const void* d_voxels, int n_img, ui
   return launch_project_generic(desc, d_voxels, s, st);
 }
 
+int dpm_project_generic(const dpm_volume_desc* desc, const void* d_voxels, int n_img, uint32_t* const* d_images,
+                        void* stream) {
+  reset_launches();
+  int rc = check_desc(desc);
+  if (rc) return rc;
+  if (n_img < 3 || n_img > DPM_MAX_IMAGES || !d_images || !d_voxels) return DPM_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ImageSet s = make_set(desc, n_img, d_images);
+  for (int k = 0; k < n_img; ++k) {
+    if (!s.img[k]) return DPM_EINVAL;
+    if (cudaMemsetAsync(s.img[k], 0, (size_t)(s.W[k] * s.H[k] * desc->B) * sizeof(uint32_t), st) != cudaSuccess)
+      return DPM_ECUDA;
+  }
+  return launch_project_generic(desc, d_voxels, s, st);
+}
+
 int dpm_moments2d(const dpm_volume_desc* desc, int n_img, const uint32_t* const* d_images, int order,
                   uint64_t* d_acc, void* stream) {
   reset_launches();

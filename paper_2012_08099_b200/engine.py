@@ -111,9 +111,14 @@ def image_layout(desc: nat.VolumeDesc, img: int) -> tuple[int, int, int, int]:
 
 def project(vox: torch.Tensor, n_img: int, offset: int = 0, z0: int = 0,
             stream: torch.cuda.Stream | None = None, imgs: list[torch.Tensor] | None = None,
-            workspace: torch.Tensor | None = None) -> list[torch.Tensor]:
+            workspace: torch.Tensor | None = None, kernel: str = "auto") -> list[torch.Tensor]:
     """Projection images 0..n_img-1 as int32 tensors [B, H, W] holding uint32
-    bits (into ``imgs`` when given, e.g. for CUDA-graph capture)."""
+    bits (into ``imgs`` when given, e.g. for CUDA-graph capture).
+
+    ``kernel``: "auto" (TMA streaming kernel where the shape allows, else the
+    generic one) or "generic" (the brick kernel only: independent cross-check)."""
+    if kernel not in ("auto", "generic"):
+        raise ValueError(f"unknown projection kernel {kernel!r}")
     desc = make_desc(vox, offset, z0)
     if imgs is None:
         imgs = []
@@ -121,6 +126,10 @@ def project(vox: torch.Tensor, n_img: int, offset: int = 0, z0: int = 0,
             W, H, _, _ = image_layout(desc, k)
             imgs.append(torch.empty((desc.B, H, W), dtype=torch.int32, device=vox.device))
     ptrs = (ctypes.c_void_p * n_img)(*[t.data_ptr() for t in imgs])
+    if kernel == "generic":
+        nat.check(nat.lib().dpm_project_generic(ctypes.byref(desc), vox.data_ptr(), n_img, ptrs,
+                                                stream_handle(stream)), "dpm_project_generic")
+        return imgs
     wsb = int(nat.lib().dpm_project_workspace_bytes(ctypes.byref(desc), n_img))
     ws = (workspace if workspace is not None else _WS.get(wsb, vox.device)) if wsb else None
     nat.check(nat.lib().dpm_project(ctypes.byref(desc), vox.data_ptr(), n_img, ptrs,

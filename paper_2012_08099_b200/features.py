@@ -135,7 +135,11 @@ def _key(pqr) -> str:
 def feature_report(volume, order: int, engine: str = "dpm", spacing=None) -> dict:
     """Moments and derived features as a deterministic JSON-ready dict with
     the reference's keys (harness.feature_report, harness.py:22-59)."""
-    tensor = ENGINES[engine](volume, order)
+    return report_from_tensor(volume, ENGINES[engine](volume, order), order, engine, spacing)
+
+
+def report_from_tensor(volume, tensor: MomentTensor3, order: int, engine: str, spacing=None) -> dict:
+    """``feature_report`` of already computed moments (e.g. a streamed file)."""
     cm = central_moments(tensor)
     eta = normalize_scale(cm)
     idx = moment_indices(order)

@@ -163,8 +163,39 @@ def dpm_moments_batch(volumes, order: int, check_consistency: bool = True, offse
     return [MomentTensor3(order, dict(zip(idx, engine.i128_to_ints(i128[b])))) for b in range(i128.shape[0])]
 
 
+def dpm_generic_moments(volume: Volume, order: int, counters: OpCounters | None = None,
+                        check_consistency: bool = True) -> MomentTensor3:
+    """The DPM pipeline with the projection pass forced through the shape-generic
+    brick kernel (``dpm_project_generic``) instead of the TMA streaming kernel;
+    2D moments and epilogue as in ``dpm_moments``.  A second, independently
+    written device projection engine, so ``harness.verify_engines`` cross-checks
+    two implementations the way the reference cross-checks its engines
+    (moments3d.py:267-271, harness.py:101-120)."""
+    import torch
+
+    from . import engine
+    from .projection import _to_device
+
+    engine.check_order(order)
+    vox = _to_device(volume)
+    dims = volume.dims if isinstance(volume, Volume) else tuple(reversed(vox.shape[-3:]))
+    engine.check_envelope(dims[0], dims[1], dims[2], nat.DPM_U8 if vox.dtype == torch.uint8 else nat.DPM_U16,
+                          order)
+    imgs = engine.project(vox, engine.num_images(order), kernel="generic")
+    acc = engine.moments2d_images(vox, imgs, order)
+    res = engine.derive(acc, order)
+    torch.cuda.current_stream().synchronize()
+    st = int(res.status[0].item())
+    if check_consistency:
+        raise_status(st, "dpm_generic")
+    vals = engine.i128_to_ints(res.i128[0].cpu().numpy())
+    _count(counters, order, dims)
+    return MomentTensor3(order, dict(zip(moment_indices(order), vals)))
+
+
 ENGINES = {
     "dpm": dpm_moments,
+    "dpm_generic": dpm_generic_moments,
 }
 
 

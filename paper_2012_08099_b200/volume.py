@@ -95,3 +95,38 @@ def ellipsoid(dims: tuple[int, int, int], center: tuple[float, float, float],
     z = (np.arange(n) - cz) / c
     inside = (z[:, None, None] ** 2 + y[None, :, None] ** 2 + x[None, None, :] ** 2) <= 1.0
     return Volume(np.where(inside, value, 0).astype(_DTYPES[bit_depth]), spacing)
+
+
+def synth(kind: str, dims: tuple[int, int, int], seed: int = 0, *, spacing=(1.0, 1.0, 1.0)) -> Volume:
+    """Synthetic volume from a descriptor (the reference CLI's ``--synth``,
+    volume.py:245-270): ``uniform:V``, ``delta:X,Y,Z,V``, ``random:BITDEPTH``,
+    ``ellipsoid:CX,CY,CZ,A,B,C[,V]``; ``seed`` only feeds ``random``."""
+    name, _, arg = kind.partition(":")
+    builders = {
+        "uniform": lambda: uniform(dims, int(arg or 1), spacing=spacing),
+        "delta": lambda: _delta_from(arg, dims, spacing),
+        "random": lambda: random(dims, int(arg or 8), seed, spacing=spacing),
+        "ellipsoid": lambda: _ellipsoid_from(arg, dims, spacing),
+    }
+    if name not in builders:
+        raise ValueError(f"unknown synth kind {name!r}")
+    try:
+        return builders[name]()
+    except ValueError as exc:
+        msg = str(exc)
+        if "outside dims" in msg or "does not fit" in msg:
+            raise
+        raise ValueError(f"malformed synth descriptor {kind!r}") from exc
+
+
+def _delta_from(arg: str, dims, spacing) -> Volume:
+    x0, y0, z0, v = (int(t) for t in arg.split(","))
+    return delta(dims, (x0, y0, z0), v, spacing=spacing)
+
+
+def _ellipsoid_from(arg: str, dims, spacing) -> Volume:
+    vals = [float(t) for t in arg.split(",")]
+    if len(vals) < 6:
+        raise ValueError("ellipsoid needs CX,CY,CZ,A,B,C")
+    value = int(vals[6]) if len(vals) > 6 else 1
+    return ellipsoid(dims, tuple(vals[0:3]), tuple(vals[3:6]), value, spacing=spacing)
