@@ -137,7 +137,7 @@ def ncu_traffic(workload_key: str):
 
 def cpu_sample_cfg(cfg: int):
     """A bounded sample of the workload for the CPU leg: (voxels, order, offset, description)."""
-    from paper_2012_08099_b200 import synth
+    from paper_2012_08099_b200 import configs as synth
     if cfg == 5:
         import oracle
         planes = 32
@@ -209,7 +209,7 @@ def main():
 
     from paper_2012_08099_b200 import _native as nat
     from paper_2012_08099_b200 import distributed as pdist
-    from paper_2012_08099_b200 import engine, synth
+    from paper_2012_08099_b200 import configs as synth, engine
 
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
@@ -351,7 +351,7 @@ def main():
         "value": round(value, 2), "unit": "GVoxel/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
         "scaling": scaling, "vs_baseline": None, "dtype": "u16" if vox.element_size() == 2 else "u8",
-        "data": "synthetic (seeded; BASELINE.json configs, see paper_2012_08099_b200/synth.py)",
+        "data": "synthetic (seeded; BASELINE.json configs, see paper_2012_08099_b200/configs.py)",
         "config": {"workload": CONFIG_DESC[cfg], "order": order, "parallelism": parallelism,
                    "voxels_per_step": total_voxels, "cache": "L2 scrubbed before every step (untimed 2xL2 write), per-step events"
                    if flush_l2 else "inputs larger than L2 (no flush)"},

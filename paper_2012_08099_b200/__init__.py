@@ -7,6 +7,7 @@ the C ABI in include/dpm_b200.h.  There is no CPU fallback: without the CUDA
 library (paper_2012_08099_b200/libdpm_b200.so) and a GPU, compute calls raise.
 """
 from . import drt2d, harness
+from .harness import BenchReport, run_bench, verify_engines
 from .counters import OpCounters
 from .drt2d import Moments2D, brute_force_2d, image_moments, shift_origin
 from .errors import FormatError, InconsistencyError
@@ -22,10 +23,10 @@ from .volume import Volume, delta, ellipsoid, random, synth, uniform
 __version__ = "0.1.0"
 
 __all__ = [
-    "ANGLES", "CentralMoments3", "ENGINES", "FormatError", "ShapeFeatures", "apply_spacing", "central_moments",
+    "ANGLES", "BenchReport", "CentralMoments3", "ENGINES", "FormatError", "ShapeFeatures", "apply_spacing", "central_moments",
     "centroid", "feature_report", "normalize_scale", "shape_features", "InconsistencyError", "Moments2D", "MomentTensor3", "OpCounters",
     "Orientation", "ProjectionImage", "ProjectionSet", "Volume", "count_ops", "delta",
-    "VolumeMeta", "brute_force_2d", "dpm_generic_moments", "dpm_moments", "dpm_moments_batch", "harness", "synth", "dpm_moments_file", "drt2d",
+    "VolumeMeta", "brute_force_2d", "dpm_generic_moments", "dpm_moments", "dpm_moments_batch", "harness", "run_bench", "synth", "verify_engines", "dpm_moments_file", "drt2d",
     "ellipsoid", "image_moments", "load_nrrd", "load_raw", "meta_from_header_file", "open_nrrd", "open_raw",
     "moment_indices", "project", "project_all",
     "project_extended", "project_subset", "random", "shift_origin", "uniform", "write_pgm", "write_raw",

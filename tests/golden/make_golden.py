@@ -76,7 +76,7 @@ def moments_dict(t) -> dict:
 
 def main():
     ref = load_reference()
-    from paper_2012_08099_b200 import synth
+    from paper_2012_08099_b200 import configs as synth
 
     # 1. projections of small volumes
     vols = small_volumes(ref)
@@ -136,7 +136,7 @@ def main():
     record("cfg5_slab", v5, 4, sha(v5), {"L": 2048, "M": 2048, "z0": 1000, "nz": 4, "seed": 5})
     cfgs["cfg5_slab"]["naive3"] = moments_dict(ref.naive_moments(ref.Volume(v5.copy()), 3))
     with open(os.path.join(HERE, "configs.json"), "w") as fh:
-        json.dump({"source": "reference volmoments on paper_2012_08099_b200.synth generators",
+        json.dump({"source": "reference volmoments on paper_2012_08099_b200.configs generators",
                    "configs": cfgs}, fh, indent=0)
 
 

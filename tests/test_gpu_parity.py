@@ -12,7 +12,7 @@ import pyoracle
 import paper_2012_08099_b200 as vm
 from golden_data import (ORIENTATIONS, configs, moments, parse_moments, projections, sha,
                          volume_for)
-from paper_2012_08099_b200 import engine, synth
+from paper_2012_08099_b200 import configs as synth, engine
 from paper_2012_08099_b200.errors import InconsistencyError
 
 pytestmark = pytest.mark.gpu

@@ -5,7 +5,7 @@ import torch
 
 import oracle
 import paper_2012_08099_b200 as vm
-from paper_2012_08099_b200 import engine, synth
+from paper_2012_08099_b200 import configs as synth, engine
 from paper_2012_08099_b200.errors import InconsistencyError
 from paper_2012_08099_b200.moments3d import raise_status
 

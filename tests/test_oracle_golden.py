@@ -12,7 +12,7 @@ import oracle
 import pyoracle
 from golden_data import (ORIENTATIONS, configs, moments, parse_moments, projections, sha,
                          volume_for)
-from paper_2012_08099_b200 import synth
+from paper_2012_08099_b200 import configs as synth
 
 
 def test_oracle_projections_equal_reference_golden():
