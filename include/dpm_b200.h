@@ -70,6 +70,10 @@ extern "C" {
 #define DPM_MAX_IMAGES 7
 #define DPM_MAX_ORDER 6
 
+/* ---- limb-accumulator kinds (what slot DPM_IMG_ZX of d_acc holds) ---------- */
+#define DPM_ACC_IMAGES 0   /* the ZX image's 2D moments (dpm_moments2d on dpm_project's images) */
+#define DPM_ACC_PROFILE 1  /* the y-summed profile's 1D moments (dpm_moments_partial, dpm_moments2d_profile) */
+
 /* A (batch of) volume(s), or a z-slab of one.  Strides are in elements. */
 typedef struct dpm_volume_desc {
   int64_t L, M, N;        /* extents along x, y, z (of this slab) */
@@ -133,16 +137,44 @@ DPM_API int dpm_moments2d(const dpm_volume_desc* desc, int n_img, const uint32_t
 DPM_API int dpm_image_moments2d(const uint32_t* d_pixels, int64_t W, int64_t H, int64_t ai, int64_t aj,
                                 int order, uint64_t* d_acc, void* stream);
 
+/* ---- the moments pipeline ------------------------------------------------
+ * dpm_moments does not build the ZX image: the q = 0 moments M_{p,0,r} come
+ * from the obliques' q = 0 rows plus ONE extra direction, the profile
+ *   P[x + t z] = sum_y V(x, y, z),  t = -1, 2, -2, 3 at orders 3, 4, 5, 6,
+ * a 1D array of WQ = L + |t|(N-1) uint64 per volume (stored index x + t z, plus
+ * |t|(N-1) when t < 0; logical coordinate = stored index + ai).  Per voxel the
+ * pass folds the profile into a register window summed over y instead of
+ * keeping the 8 x VX ZX accumulators of dpm_project.  The images it does build
+ * are bit-identical to dpm_project's. */
+DPM_API int dpm_profile_layout(const dpm_volume_desc* desc, int order, int64_t* WQ, int64_t* ai, int* t);
+/* Projection pass of the moments pipeline: images 0..num_images(order)-1
+ * except DPM_IMG_ZX (d_images[2] is ignored) plus the profile (B * WQ
+ * uint64).  Zeroes its outputs first. */
+DPM_API int dpm_project_profile(const dpm_volume_desc* desc, const void* d_voxels, int order,
+                uint32_t* const* d_images, uint64_t* d_profile, void* stream);
+/* Exact moments of those images (2D) and of the profile (1D, into the q = 0
+ * entries of slot DPM_IMG_ZX): a DPM_ACC_PROFILE accumulator, zeroed first. */
+DPM_API int dpm_moments2d_profile(const dpm_volume_desc* desc, int order, const uint32_t* const* d_images,
+                const uint64_t* d_profile, uint64_t* d_acc, void* stream);
+/* Both steps on caller scratch of dpm_partial_workspace_bytes() bytes: the
+ * per-slab partial of the multi-GPU / streaming drivers (accumulators of
+ * z-slabs taken in global coordinates add elementwise). */
+DPM_API size_t dpm_partial_workspace_bytes(const dpm_volume_desc* desc, int order);
+DPM_API int dpm_moments_partial(const dpm_volume_desc* desc, const void* d_voxels, int order,
+                void* d_ws, size_t ws_bytes, uint64_t* d_acc, void* stream);
+
 /* Device epilogue: placement + duplicate-route checks + cross-axis solve.
  * Replaces moments3d._place / _cross_axis_moments / dpm_moments:255-264
- * (moments3d.py:201-264).  Reads d_acc (as written by dpm_moments2d), writes
- * per volume n3d exact moments to d_m3d_i128 (B * n3d * 2 int64, lo/hi) and
- * fp64 copies to d_m3d_f64 (B * n3d, may be NULL), and ORs DPM_ST_* bits into
- * d_status[b] (B int32, zeroed by the call). */
-DPM_API int dpm_derive3d(const dpm_volume_desc* desc, const uint64_t* d_acc, int order,
+ * (moments3d.py:201-264).  Reads d_acc of kind `acc_kind` (DPM_ACC_IMAGES as
+ * written by dpm_moments2d, DPM_ACC_PROFILE as written by dpm_moments_partial),
+ * writes per volume n3d exact moments to d_m3d_i128 (B * n3d * 2 int64, lo/hi)
+ * and fp64 copies to d_m3d_f64 (B * n3d, may be NULL), and ORs DPM_ST_* bits
+ * into d_status[b] (B int32, zeroed by the call).  Every equation the solve
+ * does not need is checked against it (DPM_ST_DISAGREE). */
+DPM_API int dpm_derive3d(const dpm_volume_desc* desc, const uint64_t* d_acc, int order, int acc_kind,
                  int64_t* d_m3d_i128, double* d_m3d_f64, int32_t* d_status, void* stream);
 
-/* Whole pipeline (project -> 2D moments -> derive) for a volume, a batch of
+/* Whole pipeline (dpm_moments_partial -> dpm_derive3d) for a volume, a batch of
  * volumes, or a z-slab in global coordinates.  Replaces moments3d.dpm_moments
  * (moments3d.py:232-264).  Needs dpm_workspace_bytes() of scratch. */
 DPM_API size_t dpm_workspace_bytes(const dpm_volume_desc* desc, int order);
@@ -151,7 +183,8 @@ DPM_API int dpm_moments(const dpm_volume_desc* desc, const void* d_voxels, int o
                 int32_t* d_status, void* stream);
 
 /* Exactness envelope: DPM_OK when every moment of a volume/slab with the given
- * global extent and voxel maximum fits the signed 128-bit accumulators,
+ * global extent and voxel maximum fits the signed 128-bit accumulators (and,
+ * at order 6, the profile solve's intermediates: mass * max(L,M,N)^6 < 2^116),
  * else DPM_EOVERFLOW (the analogue of the reference's int64 guards,
  * moments3d.py:121-127, 158-161, drt2d.py:181-184). */
 DPM_API int dpm_check_envelope(int64_t L, int64_t M, int64_t N_global, int64_t vmax, int order);

@@ -19,6 +19,7 @@ DPM_OK, DPM_EINVAL, DPM_EOVERFLOW, DPM_ECUDA, DPM_EWORKSPACE = 0, 1, 2, 3, 4
 DPM_ST_DISAGREE, DPM_ST_NONEXACT, DPM_ST_MASS = 1, 2, 4
 DPM_U8, DPM_U16, DPM_I16 = 1, 2, 3
 MAX_IMAGES, MAX_ORDER = 7, 6
+DPM_ACC_IMAGES, DPM_ACC_PROFILE = 0, 1
 
 #: every symbol include/dpm_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = (
@@ -26,7 +27,8 @@ EXPORTS = (
     "dpm_project_workspace_bytes", "dpm_project", "dpm_moments2d", "dpm_derive3d",
     "dpm_workspace_bytes", "dpm_moments", "dpm_check_envelope", "dpm_acc_add",
     "dpm_synth_noise_u16", "dpm_last_launch_count", "dpm_strerror", "dpm_image_moments2d",
-    "dpm_project_generic",
+    "dpm_project_generic", "dpm_profile_layout", "dpm_project_profile", "dpm_moments2d_profile",
+    "dpm_partial_workspace_bytes", "dpm_moments_partial",
 )
 
 
@@ -65,7 +67,13 @@ def lib() -> ctypes.CDLL:
         "dpm_project": (ctypes.c_int, [pdesc, vp, ctypes.c_int, ctypes.POINTER(vp), vp, sz, vp]),
         "dpm_project_generic": (ctypes.c_int, [pdesc, vp, ctypes.c_int, ctypes.POINTER(vp), vp]),
         "dpm_moments2d": (ctypes.c_int, [pdesc, ctypes.c_int, ctypes.POINTER(vp), ctypes.c_int, vp, vp]),
-        "dpm_derive3d": (ctypes.c_int, [pdesc, vp, ctypes.c_int, vp, vp, vp, vp]),
+        "dpm_derive3d": (ctypes.c_int, [pdesc, vp, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp]),
+        "dpm_profile_layout": (ctypes.c_int, [pdesc, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                              ctypes.POINTER(ctypes.c_int)]),
+        "dpm_project_profile": (ctypes.c_int, [pdesc, vp, ctypes.c_int, ctypes.POINTER(vp), vp, vp]),
+        "dpm_moments2d_profile": (ctypes.c_int, [pdesc, ctypes.c_int, ctypes.POINTER(vp), vp, vp, vp]),
+        "dpm_partial_workspace_bytes": (sz, [pdesc, ctypes.c_int]),
+        "dpm_moments_partial": (ctypes.c_int, [pdesc, vp, ctypes.c_int, vp, sz, vp, vp]),
         "dpm_image_moments2d": (ctypes.c_int, [vp, i64, i64, i64, i64, ctypes.c_int, vp, vp]),
         "dpm_workspace_bytes": (sz, [pdesc, ctypes.c_int]),
         "dpm_moments": (ctypes.c_int, [pdesc, vp, ctypes.c_int, vp, sz, vp, vp, vp, vp]),

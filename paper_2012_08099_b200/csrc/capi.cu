@@ -9,12 +9,16 @@ static thread_local int g_launches = 0;
 void note_launches(int n) { g_launches += n; }
 void reset_launches() { g_launches = 0; }
 
-int launch_project_generic(const dpm_volume_desc* d, const void* vox, const ImageSet& s, cudaStream_t st);
-int launch_project_stream(const dpm_volume_desc* d, const void* vox, const ImageSet& s, void* ws, size_t ws_bytes,
+int launch_project_generic(const dpm_volume_desc* d, const void* vox, const ImageSet& s, unsigned long long* prof,
+                           cudaStream_t st);
+int launch_project_stream(const dpm_volume_desc* d, const void* vox, const ImageSet& s, unsigned long long* prof,
                           cudaStream_t st, bool* handled);
+int profile_shift(int n_img);
 size_t project_stream_workspace(const dpm_volume_desc* d, int n_img);
 int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_t* acc, cudaStream_t st);
-int launch_derive3d(const uint64_t* acc, int64_t B, int n_img, int order, int64_t* out_i128,
+int launch_profile_moments(const unsigned long long* prof, int64_t WQ, int64_t B, int64_t ai, int order, int n_img,
+                           int slot, uint64_t* acc, cudaStream_t st);
+int launch_derive3d(const uint64_t* acc, int64_t B, int n_img, int order, int kind, int64_t* out_i128,
                     double* out_f64, int32_t* status, cudaStream_t st);
 int launch_synth_noise(uint16_t* out, int64_t L, int64_t M, int64_t z0, int64_t nz, uint64_t seed, cudaStream_t st);
 
@@ -37,11 +41,13 @@ static int check_desc(const dpm_volume_desc* d) {
 
 static int check_order(int order) { return (order >= 3 && order <= DPM_MAX_ORDER) ? DPM_OK : DPM_EINVAL; }
 
-static ImageSet make_set(const dpm_volume_desc* d, int n_img, uint32_t* const* imgs) {
+// no_zx: moments-pipeline image set (slot 2 empty: W = H = 0, no pointer)
+static ImageSet make_set(const dpm_volume_desc* d, int n_img, uint32_t* const* imgs, bool no_zx = false) {
   ImageSet s;
   memset(&s, 0, sizeof(s));
   s.n_img = n_img;
   for (int k = 0; k < n_img; ++k) {
+    if (no_zx && k == DPM_IMG_ZX) continue;
     const ImageGeom g = image_geom(d->L, d->M, d->N, d->z0, k);
     s.img[k] = imgs ? imgs[k] : nullptr;
     s.W[k] = g.W; s.H[k] = g.H; s.ai[k] = g.ai; s.aj[k] = g.aj;
@@ -51,14 +57,27 @@ static ImageSet make_set(const dpm_volume_desc* d, int n_img, uint32_t* const* i
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-static size_t images_bytes(const dpm_volume_desc* d, int n_img, size_t* offs) {
+static size_t images_bytes(const dpm_volume_desc* d, int n_img, size_t* offs, bool no_zx = false) {
   size_t total = 0;
   for (int k = 0; k < n_img; ++k) {
     const ImageGeom g = image_geom(d->L, d->M, d->N, d->z0, k);
     if (offs) offs[k] = total;
+    if (no_zx && k == DPM_IMG_ZX) continue;
     total += align256((size_t)(g.W * g.H * d->B) * sizeof(uint32_t));
   }
   return total;
+}
+
+// the y-summed profile of the moments pipeline: direction t, stored length WQ,
+// logical coordinate = stored index + ai (global z: ai includes t * z0)
+struct ProfGeom { int t; int64_t WQ, ai; };
+static ProfGeom profile_geom(const dpm_volume_desc* d, int order) {
+  ProfGeom g;
+  g.t = profile_shift(num_images(order));
+  const int64_t at = g.t < 0 ? -g.t : g.t;
+  g.WQ = d->L + at * (d->N - 1);
+  g.ai = g.t > 0 ? g.t * d->z0 : -at * (d->N - 1) - at * d->z0;
+  return g;
 }
 
 static int jbits_for(const dpm_volume_desc* d, int n_img) {
@@ -110,10 +129,11 @@ int dpm_project(const dpm_volume_desc* desc, const void* d_voxels, int n_img, ui
     if (cudaMemsetAsync(s.img[k], 0, (size_t)(s.W[k] * s.H[k] * desc->B) * sizeof(uint32_t), st) != cudaSuccess)
       return DPM_ECUDA;
   }
+  (void)d_ws; (void)ws_bytes;
   bool handled = false;
-  rc = launch_project_stream(desc, d_voxels, s, d_ws, ws_bytes, st, &handled);
+  rc = launch_project_stream(desc, d_voxels, s, nullptr, st, &handled);
   if (rc || handled) return rc;
-  return launch_project_generic(desc, d_voxels, s, st);
+  return launch_project_generic(desc, d_voxels, s, nullptr, st);
 }
 
 int dpm_project_generic(const dpm_volume_desc* desc, const void* d_voxels, int n_img, uint32_t* const* d_images,
@@ -129,7 +149,90 @@ int dpm_project_generic(const dpm_volume_desc* desc, const void* d_voxels, int n
     if (cudaMemsetAsync(s.img[k], 0, (size_t)(s.W[k] * s.H[k] * desc->B) * sizeof(uint32_t), st) != cudaSuccess)
       return DPM_ECUDA;
   }
-  return launch_project_generic(desc, d_voxels, s, st);
+  return launch_project_generic(desc, d_voxels, s, nullptr, st);
+}
+
+int dpm_profile_layout(const dpm_volume_desc* desc, int order, int64_t* WQ, int64_t* ai, int* t) {
+  if (check_desc(desc) || check_order(order)) return DPM_EINVAL;
+  const ProfGeom g = profile_geom(desc, order);
+  if (WQ) *WQ = g.WQ;
+  if (ai) *ai = g.ai;
+  if (t) *t = g.t;
+  return DPM_OK;
+}
+
+int dpm_project_profile(const dpm_volume_desc* desc, const void* d_voxels, int order, uint32_t* const* d_images,
+                        uint64_t* d_profile, void* stream) {
+  reset_launches();
+  int rc = check_desc(desc);
+  if (rc) return rc;
+  if (check_order(order) || !d_images || !d_voxels || !d_profile) return DPM_EINVAL;
+  const int n_img = num_images(order);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ImageSet s = make_set(desc, n_img, d_images, true);
+  for (int k = 0; k < n_img; ++k) {
+    if (k == DPM_IMG_ZX) continue;
+    if (!s.img[k]) return DPM_EINVAL;
+    if (cudaMemsetAsync(s.img[k], 0, (size_t)(s.W[k] * s.H[k] * desc->B) * sizeof(uint32_t), st) != cudaSuccess)
+      return DPM_ECUDA;
+  }
+  const ProfGeom pg = profile_geom(desc, order);
+  if (cudaMemsetAsync(d_profile, 0, (size_t)(pg.WQ * desc->B) * sizeof(uint64_t), st) != cudaSuccess) return DPM_ECUDA;
+  unsigned long long* prof = reinterpret_cast<unsigned long long*>(d_profile);
+  bool handled = false;
+  rc = launch_project_stream(desc, d_voxels, s, prof, st, &handled);
+  if (rc || handled) return rc;
+  return launch_project_generic(desc, d_voxels, s, prof, st);
+}
+
+int dpm_moments2d_profile(const dpm_volume_desc* desc, int order, const uint32_t* const* d_images,
+                          const uint64_t* d_profile, uint64_t* d_acc, void* stream) {
+  reset_launches();
+  int rc = check_desc(desc);
+  if (rc) return rc;
+  if (check_order(order) || !d_images || !d_profile || !d_acc) return DPM_EINVAL;
+  const int n_img = num_images(order);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ImageSet s = make_set(desc, n_img, const_cast<uint32_t* const*>(d_images), true);
+  const int jb = jbits_for(desc, n_img);
+  if (jb > 21) return DPM_EOVERFLOW;
+  if (cudaMemsetAsync(d_acc, 0, (size_t)(desc->B * n_img * n2d(order) * 4) * sizeof(uint64_t), st) != cudaSuccess)
+    return DPM_ECUDA;
+  rc = launch_moments2d(s, desc->B, order, jb, d_acc, st);
+  if (rc) return rc;
+  const ProfGeom pg = profile_geom(desc, order);
+  rc = launch_profile_moments(reinterpret_cast<const unsigned long long*>(d_profile), pg.WQ, desc->B, pg.ai, order,
+                              n_img, DPM_IMG_ZX, d_acc, st);
+  return rc;
+}
+
+size_t dpm_partial_workspace_bytes(const dpm_volume_desc* desc, int order) {
+  if (check_desc(desc) || check_order(order)) return 0;
+  const ProfGeom pg = profile_geom(desc, order);
+  return images_bytes(desc, num_images(order), nullptr, true) + align256((size_t)(pg.WQ * desc->B) * sizeof(uint64_t));
+}
+
+int dpm_moments_partial(const dpm_volume_desc* desc, const void* d_voxels, int order, void* d_ws, size_t ws_bytes,
+                        uint64_t* d_acc, void* stream) {
+  int rc = check_desc(desc);
+  if (rc) return rc;
+  if (check_order(order) || !d_voxels || !d_acc) return DPM_EINVAL;
+  if (ws_bytes < dpm_partial_workspace_bytes(desc, order) || !d_ws) return DPM_EWORKSPACE;
+  const int n_img = num_images(order);
+  size_t offs[DPM_MAX_IMAGES];
+  const size_t ib = images_bytes(desc, n_img, offs, true);
+  uint32_t* imgs[DPM_MAX_IMAGES];
+  char* base = static_cast<char*>(d_ws);
+  for (int k = 0; k < n_img; ++k) imgs[k] = k == DPM_IMG_ZX ? nullptr : reinterpret_cast<uint32_t*>(base + offs[k]);
+  uint64_t* prof = reinterpret_cast<uint64_t*>(base + ib);
+  int launches = 0;
+  rc = dpm_project_profile(desc, d_voxels, order, imgs, prof, stream);
+  launches += dpm_last_launch_count();
+  if (rc) return rc;
+  rc = dpm_moments2d_profile(desc, order, imgs, prof, d_acc, stream);
+  launches += dpm_last_launch_count();
+  g_launches = launches;
+  return rc;
 }
 
 int dpm_moments2d(const dpm_volume_desc* desc, int n_img, const uint32_t* const* d_images, int order,
@@ -163,21 +266,20 @@ int dpm_image_moments2d(const uint32_t* d_pixels, int64_t W, int64_t H, int64_t 
   return launch_moments2d(s, 1, order, jb, d_acc, st);
 }
 
-int dpm_derive3d(const dpm_volume_desc* desc, const uint64_t* d_acc, int order, int64_t* d_m3d_i128,
+int dpm_derive3d(const dpm_volume_desc* desc, const uint64_t* d_acc, int order, int acc_kind, int64_t* d_m3d_i128,
                  double* d_m3d_f64, int32_t* d_status, void* stream) {
   reset_launches();
   if (!desc || desc->B < 1 || check_order(order) || !d_acc || !d_m3d_i128 || !d_status) return DPM_EINVAL;
-  return launch_derive3d(d_acc, desc->B, num_images(order), order, d_m3d_i128, d_m3d_f64, d_status,
+  if (acc_kind != DPM_ACC_IMAGES && acc_kind != DPM_ACC_PROFILE) return DPM_EINVAL;
+  return launch_derive3d(d_acc, desc->B, num_images(order), order, acc_kind, d_m3d_i128, d_m3d_f64, d_status,
                          static_cast<cudaStream_t>(stream));
 }
 
 size_t dpm_workspace_bytes(const dpm_volume_desc* desc, int order) {
   if (check_desc(desc) || check_order(order)) return 0;
   const int n_img = num_images(order);
-  size_t total = images_bytes(desc, n_img, nullptr);
-  total += align256((size_t)(desc->B * n_img * n2d(order) * 4) * sizeof(uint64_t));
-  total += align256(project_stream_workspace(desc, n_img));
-  return total;
+  return align256((size_t)(desc->B * n_img * n2d(order) * 4) * sizeof(uint64_t)) +
+         dpm_partial_workspace_bytes(desc, order);
 }
 
 int dpm_check_envelope(int64_t L, int64_t M, int64_t N_global, int64_t vmax, int order) {
@@ -187,7 +289,16 @@ int dpm_check_envelope(int64_t L, int64_t M, int64_t N_global, int64_t vmax, int
   const int64_t cmax = imax64(imax64(L, M), L + 2 * N_global);
   long double bound = mass;
   for (int k = 0; k < order; ++k) bound *= (long double)cmax;
-  return bound < 0x1p126L ? DPM_OK : DPM_EOVERFLOW;
+  if (bound >= 0x1p126L) return DPM_EOVERFLOW;
+  if (order == 6) {
+    // the order-6 profile solve (derive3d, five unknowns) forms sums of up to
+    // 2016 x the largest 3D moment: keep mass * max(L, M, N)^6 < 2^116
+    const int64_t c3 = imax64(imax64(L, M), N_global);
+    long double b6 = mass;
+    for (int k = 0; k < 6; ++k) b6 *= (long double)c3;
+    if (b6 >= 0x1p116L) return DPM_EOVERFLOW;
+  }
+  return DPM_OK;
 }
 
 int dpm_moments(const dpm_volume_desc* desc, const void* d_voxels, int order, void* d_ws, size_t ws_bytes,
@@ -197,23 +308,14 @@ int dpm_moments(const dpm_volume_desc* desc, const void* d_voxels, int order, vo
   if (check_order(order) || !d_voxels || !d_m3d_i128 || !d_status) return DPM_EINVAL;
   if (ws_bytes < dpm_workspace_bytes(desc, order) || !d_ws) return DPM_EWORKSPACE;
   const int n_img = num_images(order);
-  size_t offs[DPM_MAX_IMAGES];
-  const size_t ib = images_bytes(desc, n_img, offs);
-  uint32_t* imgs[DPM_MAX_IMAGES];
-  char* base = static_cast<char*>(d_ws);
-  for (int k = 0; k < n_img; ++k) imgs[k] = reinterpret_cast<uint32_t*>(base + offs[k]);
-  uint64_t* acc = reinterpret_cast<uint64_t*>(base + ib);
+  uint64_t* acc = static_cast<uint64_t*>(d_ws);
   const size_t acc_bytes = align256((size_t)(desc->B * n_img * n2d(order) * 4) * sizeof(uint64_t));
-  void* pws = base + ib + acc_bytes;
-  const size_t pws_bytes = ws_bytes - ib - acc_bytes;
   int launches = 0;
-  rc = dpm_project(desc, d_voxels, n_img, imgs, pws, pws_bytes, stream);
+  rc = dpm_moments_partial(desc, d_voxels, order, static_cast<char*>(d_ws) + acc_bytes, ws_bytes - acc_bytes, acc,
+                           stream);
   launches += dpm_last_launch_count();
   if (rc) return rc;
-  rc = dpm_moments2d(desc, n_img, imgs, order, acc, stream);
-  launches += dpm_last_launch_count();
-  if (rc) return rc;
-  rc = dpm_derive3d(desc, acc, order, d_m3d_i128, d_m3d_f64, d_status, stream);
+  rc = dpm_derive3d(desc, acc, order, DPM_ACC_PROFILE, d_m3d_i128, d_m3d_f64, d_status, stream);
   launches += dpm_last_launch_count();
   g_launches = launches;
   return rc;

@@ -8,8 +8,17 @@
 // solved in closed form (exact integer divisions).  At order 4 these are the
 // reference's formulas (moments3d.py:213-219; note the oracle-pinned sum/
 // difference association, test_moments3d.py:116-147).  Orders 5-6 extend the
-// same scheme.  One warp per volume; the placement and
-// the independent solve groups are spread over its lanes.
+// same scheme.
+//
+// Accumulator kinds.  DPM_ACC_IMAGES: slot 2 holds the ZX image's moments
+// (dpm_moments2d over the reference's image set).  DPM_ACC_PROFILE (the
+// moments pipeline): slot 2 holds the 1D moments of the y-summed profile
+// P[x + t z], t = profile_shift (-1, 2, -2, 3 at orders 3..6), so the q = 0
+// family M_{p,0,r} (p, r >= 1) is solved like the others, from the obliques'
+// q = 0 rows plus the profile as the next direction t (order 6, p + r = 6:
+// five unknowns from t = 1, -1, 2, -2, 3).  Every equation a group does not
+// need is checked against the solution (DPM_ST_DISAGREE), including the
+// p + r = 1 rows, which have no unknowns at all.
 #include "dpm_common.cuh"
 
 namespace dpm {
@@ -67,7 +76,7 @@ __constant__ int64_t kBinom[7][7] = {{1, 0, 0, 0, 0, 0, 0},  {1, 1, 0, 0, 0, 0, 
                                      {1, 3, 3, 1, 0, 0, 0},  {1, 4, 6, 4, 1, 0, 0},   {1, 5, 10, 10, 5, 1, 0},
                                      {1, 6, 15, 20, 15, 6, 1}};
 
-constexpr int kDeriveWarps = 16;   // >= the 10 solve groups of order 6
+constexpr int kDeriveWarps = 16;   // solve/check groups (<= 21 at order 6) are dealt round-robin
 
 // One CTA per volume.  The volume's limb accumulator (n_img x n2d x 4 words,
 // <= 6.3 KB) is staged in shared memory by one coalesced load; threads then
@@ -78,8 +87,9 @@ constexpr int kDeriveWarps = 16;   // >= the 10 solve groups of order 6
 // lane divergence.
 template <int K>
 __global__ void __launch_bounds__(32 * kDeriveWarps) derive3d_kernel(const uint64_t* acc, int64_t B, int n_img,
-                                                                    int64_t* out_i128, double* out_f64,
+                                                                    int kind, int64_t* out_i128, double* out_f64,
                                                                     int32_t* status) {
+  const bool prof = kind == DPM_ACC_PROFILE;
   constexpr int N2 = (K + 1) * (K + 2) / 2;
   constexpr int N3 = (K + 1) * (K + 2) * (K + 3) / 6;
   __shared__ uint64_t sa[DPM_MAX_IMAGES * N2 * 4];
@@ -106,7 +116,7 @@ __global__ void __launch_bounds__(32 * kDeriveWarps) derive3d_kernel(const uint6
     for (int p = 0; p <= K; ++p)
       for (int q = 0; q <= K - p; ++q)
         for (int r = 0; r <= K - p - q; ++r, ++n) {
-          if (n % (32 * kDeriveWarps) != tid || (p > 0 && q > 0 && r > 0)) continue;
+          if (n % (32 * kDeriveWarps) != tid || (p > 0 && r > 0 && (q > 0 || prof))) continue;
           bool have = false;
           i128 v = 0;
           auto route = [&](i128 x) {
@@ -115,30 +125,36 @@ __global__ void __launch_bounds__(32 * kDeriveWarps) derive3d_kernel(const uint6
           };
           if (r == 0) route(m2(DPM_IMG_XY, p, q));
           if (p == 0) route(m2(DPM_IMG_YZ, q, r));
-          if (q == 0) route(m2(DPM_IMG_ZX, r, p));
+          if (q == 0 && !prof) route(m2(DPM_IMG_ZX, r, p));
           put(n, v);
         }
   }
 
-  // cross-axis groups
+  // cross-axis groups (q, a = p + r): unknowns u_c = C(a,c) M_{a-c,q,c}, c = 1..a-1, from
+  //   f_t = M^t_{a,q} - M_{a,q,0} - t^a M_{0,q,a} = sum_c t^c u_c
+  // over the oblique images t = 1, -1, 2, -2 (and, for q = 0 in profile mode,
+  // the profile as the next t).  Groups with a = 1 only check.
   if (lane == 0) {
-    const int tv[4] = {1, -1, 2, -2};
+    const int tv[5] = {1, -1, 2, -2, 3};
+    const int n_obl = n_img - 3;
     int g = 0;
-    for (int q = 1; q <= K - 2; ++q)
-      for (int p = 2; p <= K - q; ++p, ++g) {
+    for (int q = prof ? 0 : 1; q <= K - 1; ++q)
+      for (int p = 1; p <= K - q; ++p, ++g) {
         if (g % kDeriveWarps != w) continue;
-        const int n = p - 1;
+        const int n = p - 1;                               // unknowns
+        const int avail = (q == 0) ? n_obl + 1 : n_obl;    // equations (q = 0 only in profile mode)
         const i128 mxy = m2(DPM_IMG_XY, p, q), myz = m2(DPM_IMG_YZ, q, p);
-        i128 f[4] = {0, 0, 0, 0};
+        i128 f[5] = {0, 0, 0, 0, 0};
         #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (k < n) {
+        for (int k = 0; k < 5; ++k) {
+          if (k < avail) {
             i128 tp = 1;
             for (int e = 0; e < p; ++e) tp *= tv[k];
-            f[k] = m2(DPM_IMG_DIAG + k, p, q) - mxy - tp * myz;
+            const int slot = k < n_obl ? DPM_IMG_DIAG + k : DPM_IMG_ZX;   // profile in the ZX slot
+            f[k] = m2(slot, p, q) - mxy - tp * myz;
           }
         }
-        i128 u[5] = {0, 0, 0, 0, 0};
+        i128 u[6] = {0, 0, 0, 0, 0, 0};
         bool ok = true;
         if (n == 1) {
           u[1] = f[0];
@@ -150,15 +166,35 @@ __global__ void __launch_bounds__(32 * kDeriveWarps) derive3d_kernel(const uint6
           ok &= div_exact(S, 2, &u[2]);
           ok &= div_exact(f[2] - 2 * S - D, 6, &u[3]);
           i128 h; ok &= div_exact(D, 2, &h); u[1] = h - u[3];
-        } else {
+        } else if (n >= 4) {
           i128 E1, E2, O1, O2;
           ok &= div_exact(f[0] + f[1], 2, &E1); ok &= div_exact(f[2] + f[3], 2, &E2);
           ok &= div_exact(f[0] - f[1], 2, &O1); ok &= div_exact(f[2] - f[3], 2, &O2);
           ok &= div_exact(E2 - 4 * E1, 12, &u[4]); u[2] = E1 - u[4];
-          ok &= div_exact(O2 - 2 * O1, 6, &u[3]); u[1] = O1 - u[3];
+          if (n == 4) {
+            ok &= div_exact(O2 - 2 * O1, 6, &u[3]); u[1] = O1 - u[3];
+          } else {   // n == 5: odd unknowns u1, u3, u5 from t = +-1, +-2 and 3
+            i128 P2, F, A3, B5;
+            ok &= div_exact(O2, 2, &P2);                              // u1 + 4 u3 + 16 u5
+            ok &= div_exact(f[4] - 9 * u[2] - 81 * u[4], 3, &F);      // u1 + 9 u3 + 81 u5
+            ok &= div_exact(P2 - O1, 3, &A3);                         // u3 + 5 u5
+            ok &= div_exact(F - P2, 5, &B5);                          // u3 + 13 u5
+            ok &= div_exact(B5 - A3, 8, &u[5]);
+            u[3] = A3 - 5 * u[5];
+            u[1] = O1 - u[3] - u[5];
+          }
+        }
+        // equations the solve did not use must agree with it
+        #pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          if (k >= n && k < avail) {
+            i128 pred = 0, tc = 1;
+            for (int c = 1; c <= n; ++c) { tc *= tv[k]; pred += tc * u[c]; }
+            if (pred != f[k]) st |= DPM_ST_DISAGREE;
+          }
         }
         #pragma unroll
-        for (int c = 1; c <= 4; ++c) {
+        for (int c = 1; c <= 5; ++c) {
           if (c <= n) {
             i128 m = 0;
             ok &= div_exact(u[c], kBinom[p][c], &m);
@@ -174,15 +210,15 @@ __global__ void __launch_bounds__(32 * kDeriveWarps) derive3d_kernel(const uint6
   if (tid == 0) status[b] = sst;
 }
 
-int launch_derive3d(const uint64_t* acc, int64_t B, int n_img, int order, int64_t* out_i128,
+int launch_derive3d(const uint64_t* acc, int64_t B, int n_img, int order, int kind, int64_t* out_i128,
                     double* out_f64, int32_t* status, cudaStream_t st) {
   const int threads = 32 * kDeriveWarps;   // one CTA per volume
   const unsigned grid = (unsigned)B;
   switch (order) {
-    case 3: derive3d_kernel<3><<<grid, threads, 0, st>>>(acc, B, n_img, out_i128, out_f64, status); break;
-    case 4: derive3d_kernel<4><<<grid, threads, 0, st>>>(acc, B, n_img, out_i128, out_f64, status); break;
-    case 5: derive3d_kernel<5><<<grid, threads, 0, st>>>(acc, B, n_img, out_i128, out_f64, status); break;
-    default: derive3d_kernel<6><<<grid, threads, 0, st>>>(acc, B, n_img, out_i128, out_f64, status); break;
+    case 3: derive3d_kernel<3><<<grid, threads, 0, st>>>(acc, B, n_img, kind, out_i128, out_f64, status); break;
+    case 4: derive3d_kernel<4><<<grid, threads, 0, st>>>(acc, B, n_img, kind, out_i128, out_f64, status); break;
+    case 5: derive3d_kernel<5><<<grid, threads, 0, st>>>(acc, B, n_img, kind, out_i128, out_f64, status); break;
+    default: derive3d_kernel<6><<<grid, threads, 0, st>>>(acc, B, n_img, kind, out_i128, out_f64, status); break;
   }
   note_launches(1);
   DPM_CUDA_CHECK_LAUNCH();

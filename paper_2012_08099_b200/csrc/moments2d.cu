@@ -209,4 +209,65 @@ int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_
   return DPM_OK;
 }
 
+// 1D exact moments of the y-summed profile (moments pipeline, DPM_ACC_PROFILE):
+//   M_a = sum_i P[i] (i + ai)^a,  a = 0..K,
+// into the q = 0 entries of accumulator slot `slot` ([B][n_img][n2d][4] limb
+// sums, zeroed by the caller).  Each term is formed mod 2^128 and split into
+// four 32-bit limbs summed in uint64, as in moments2d_kernel.
+constexpr int PM_THREADS = 256;
+
+template <int K>
+__global__ void __launch_bounds__(PM_THREADS) profile_moments_kernel(const unsigned long long* prof, int64_t WQ,
+                                                                    int64_t B, int64_t ai, int n_img, int slot,
+                                                                    uint64_t* acc) {
+  constexpr int N2 = (K + 1) * (K + 2) / 2;
+  for (int64_t b = blockIdx.y; b < B; b += gridDim.y) {
+  uint64_t l[K + 1][4];
+  #pragma unroll
+  for (int a = 0; a <= K; ++a) { l[a][0] = l[a][1] = l[a][2] = l[a][3] = 0; }
+  for (int64_t i = (int64_t)blockIdx.x * PM_THREADS + threadIdx.x; i < WQ; i += (int64_t)gridDim.x * PM_THREADS) {
+    const unsigned long long v = prof[b * WQ + i];
+    if (v == 0) continue;
+    const __int128 x = (__int128)(i + ai);
+    __int128 pw = 1;
+    #pragma unroll
+    for (int a = 0; a <= K; ++a) {
+      const unsigned __int128 t = (unsigned __int128)v * (unsigned __int128)pw;
+      l[a][0] += (uint32_t)t;
+      l[a][1] += (uint32_t)(t >> 32);
+      l[a][2] += (uint32_t)(t >> 64);
+      l[a][3] += (uint32_t)(t >> 96);
+      pw *= x;
+    }
+  }
+  uint64_t* out = acc + ((b * n_img + slot) * N2) * 4;
+  #pragma unroll
+  for (int a = 0; a <= K; ++a) {
+    #pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint64_t v = l[a][k];
+      #pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if ((threadIdx.x & 31) == 0 && v) atomicAdd(reinterpret_cast<unsigned long long*>(out + idx2(K, a, 0) * 4 + k),
+                                                  (unsigned long long)v);
+    }
+  }
+  }
+}
+
+int launch_profile_moments(const unsigned long long* prof, int64_t WQ, int64_t B, int64_t ai, int order, int n_img,
+                           int slot, uint64_t* acc, cudaStream_t st) {
+  const unsigned gx = (unsigned)imin64((WQ + PM_THREADS - 1) / PM_THREADS, 64);
+  const dim3 grid(gx, (unsigned)imin64(B, 65535));
+  switch (order) {
+    case 3: profile_moments_kernel<3><<<grid, PM_THREADS, 0, st>>>(prof, WQ, B, ai, n_img, slot, acc); break;
+    case 4: profile_moments_kernel<4><<<grid, PM_THREADS, 0, st>>>(prof, WQ, B, ai, n_img, slot, acc); break;
+    case 5: profile_moments_kernel<5><<<grid, PM_THREADS, 0, st>>>(prof, WQ, B, ai, n_img, slot, acc); break;
+    default: profile_moments_kernel<6><<<grid, PM_THREADS, 0, st>>>(prof, WQ, B, ai, n_img, slot, acc); break;
+  }
+  note_launches(1);
+  DPM_CUDA_CHECK_LAUNCH();
+  return DPM_OK;
+}
+
 }  // namespace dpm

@@ -13,6 +13,7 @@ namespace dpm {
 constexpr int GBX = 64, GBY = 4, GBZ = 16;
 constexpr int GW1 = GBX + GBZ - 1;        // DIAG/ANTI brick footprint width
 constexpr int GW2 = GBX + 2 * GBZ - 2;    // X2P/X2M brick footprint width
+constexpr int GWQ = GBX + 3 * (GBZ - 1);  // profile footprint width (|t| <= 3)
 
 struct GenericParams {
   const void* vox;
@@ -21,6 +22,10 @@ struct GenericParams {
   int32_t offset;
   int64_t nbx, nby, nbz;
   ImageSet s;
+  // moments mode: profile P[x + tq z] summed over y (uint64 [B][WQ]) instead of ZX
+  unsigned long long* prof;
+  int tq;
+  int64_t WQ, qoff;
 };
 
 template <typename T>
@@ -31,7 +36,10 @@ __global__ void __launch_bounds__(256) project_generic_kernel(GenericParams p) {
   __shared__ uint32_t an_s[GBY][GW1];
   __shared__ uint32_t xp_s[GBY][GW2];
   __shared__ uint32_t xm_s[GBY][GW2];
+  __shared__ uint32_t pq_s[GWQ];
   const int n_img = p.s.n_img;
+  const bool prof = p.prof != nullptr;
+  const int aq = p.tq < 0 ? -p.tq : p.tq;
   const int tid = threadIdx.x;
   const int xl = tid % GBX, yl = tid / GBX;
   const int64_t bricks_per_vol = p.nbx * p.nby * p.nbz;
@@ -48,6 +56,7 @@ __global__ void __launch_bounds__(256) project_generic_kernel(GenericParams p) {
 
     for (int i = tid; i < GBZ * GBY; i += blockDim.x) (&yz_s[0][0])[i] = 0;
     for (int i = tid; i < GBX * (GBZ + 1); i += blockDim.x) (&zx_s[0][0])[i] = 0;
+    for (int i = tid; i < GWQ; i += blockDim.x) pq_s[i] = 0;
     for (int i = tid; i < GBY * GW1; i += blockDim.x) { (&dg_s[0][0])[i] = 0; (&an_s[0][0])[i] = 0; }
     for (int i = tid; i < GBY * GW2; i += blockDim.x) { (&xp_s[0][0])[i] = 0; (&xm_s[0][0])[i] = 0; }
     __syncthreads();
@@ -65,7 +74,8 @@ __global__ void __launch_bounds__(256) project_generic_kernel(GenericParams p) {
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if ((tid & 31) == 0 && s) atomicAdd(&yz_s[zl][yl], s);
       if (v) {
-        atomicAdd(&zx_s[xl][zl], v);
+        if (prof) atomicAdd(&pq_s[p.tq > 0 ? xl + p.tq * zl : xl + aq * (GBZ - 1 - zl)], v);
+        else atomicAdd(&zx_s[xl][zl], v);
         atomicAdd(&dg_s[yl][xl + zl], v);
         if (n_img > DPM_IMG_ANTI) atomicAdd(&an_s[yl][xl - zl + GBZ - 1], v);
         if (n_img > DPM_IMG_X2P) atomicAdd(&xp_s[yl][xl + 2 * zl], v);
@@ -81,10 +91,19 @@ __global__ void __launch_bounds__(256) project_generic_kernel(GenericParams p) {
       const uint32_t v = yz_s[zl][yy];
       if (v) atomicAdd(p.s.img[DPM_IMG_YZ] + b * p.s.W[1] * p.s.H[1] + (z0 + zl) * p.M + (y0 + yy), v);
     }
-    for (int i = tid; i < GBX * GBZ; i += blockDim.x) {
-      const int xx = i / GBZ, zl = i % GBZ;
-      const uint32_t v = zx_s[xx][zl];
-      if (v) atomicAdd(p.s.img[DPM_IMG_ZX] + b * p.s.W[2] * p.s.H[2] + (x0 + xx) * p.N + (z0 + zl), v);
+    if (prof) {
+      // local d -> stored x + tq z (tq > 0) or x - |tq| z + qoff (tq < 0)
+      const int64_t g0 = p.tq > 0 ? x0 + p.tq * z0 : x0 - aq * (GBZ - 1) - aq * z0 + p.qoff;
+      for (int i = tid; i < GWQ; i += blockDim.x) {
+        const uint32_t v = pq_s[i];
+        if (v) atomicAdd(p.prof + b * p.WQ + g0 + i, (unsigned long long)v);
+      }
+    } else {
+      for (int i = tid; i < GBX * GBZ; i += blockDim.x) {
+        const int xx = i / GBZ, zl = i % GBZ;
+        const uint32_t v = zx_s[xx][zl];
+        if (v) atomicAdd(p.s.img[DPM_IMG_ZX] + b * p.s.W[2] * p.s.H[2] + (x0 + xx) * p.N + (z0 + zl), v);
+      }
     }
     for (int i = tid; i < GBY * GW1; i += blockDim.x) {
       const int yy = i / GW1, d = i % GW1;
@@ -114,8 +133,19 @@ __global__ void __launch_bounds__(256) project_generic_kernel(GenericParams p) {
   }
 }
 
-int launch_project_generic(const dpm_volume_desc* d, const void* vox, const ImageSet& s, cudaStream_t st) {
+int profile_shift(int n_img);
+
+// prof != nullptr: moments mode (the profile along x + t z replaces ZX)
+int launch_project_generic(const dpm_volume_desc* d, const void* vox, const ImageSet& s, unsigned long long* prof,
+                           cudaStream_t st) {
   GenericParams p;
+  p.prof = prof;
+  p.tq = profile_shift(s.n_img);
+  {
+    const int at = p.tq < 0 ? -p.tq : p.tq;
+    p.WQ = d->L + at * (d->N - 1);
+    p.qoff = p.tq < 0 ? at * (d->N - 1) : 0;
+  }
   p.vox = vox; p.L = d->L; p.M = d->M; p.N = d->N; p.B = d->B;
   p.sy = d->stride_y; p.sz = d->stride_z; p.sb = d->stride_b; p.offset = d->offset;
   p.nbx = (d->L + GBX - 1) / GBX; p.nby = (d->M + GBY - 1) / GBY; p.nbz = (d->N + GBZ - 1) / GBZ;

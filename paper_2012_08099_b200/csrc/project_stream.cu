@@ -49,6 +49,17 @@
 
 namespace dpm {
 
+// Pipe balance.  The fold adds are 3-input IADD3 on the ALU pipe; a window
+// listed in DPM_FMA_FOLDS (bit 0 DIAG, 1 ANTI, 2 X2P, 3 X2M, 4 profile) is
+// folded with single IMAD-by-1 adds on the otherwise idle FMA pipe instead.
+#ifndef DPM_FMA_FOLDS
+#define DPM_FMA_FOLDS 16
+#endif
+// DPM_UNPACK_MIX: 16-bit unpack as hi = SHF (ALU), lo = IMAD (FMA) instead of LOP3 + SHF
+#ifndef DPM_UNPACK_MIX
+#define DPM_UNPACK_MIX 0
+#endif
+
 struct StreamParams {
   int64_t L, M, N, B;
   int32_t offset;
@@ -56,7 +67,16 @@ struct StreamParams {
   int64_t band;                // rows per y-band
   uint32_t one;                // == 1 at run time: keeps the ZX adds on the FMA pipe (IMAD)
   ImageSet s;
+  // profile mode: the y-summed profile P[x + t z] (uint64 [B][WQ]) replaces
+  // the ZX image; qoff = |t| (N - 1) for t < 0, else 0
+  unsigned long long* prof;
+  int64_t WQ, qoff;
 };
+
+// Profile direction t of the moments pass (x + t z, summed over y), by image
+// count: the next (x, z) direction after the oblique images of the order --
+// order 3: -1, order 4: 2, order 5: -2, order 6: 3 ("profile").
+template <int NI> struct ProfT { static constexpr int value = NI <= 4 ? -1 : NI == 5 ? 2 : NI == 6 ? -2 : 3; };
 
 // ---- VX-voxel lane vectors --------------------------------------------------
 template <typename T, int VX> struct Vec;
@@ -69,10 +89,13 @@ template <> struct Vec<uint8_t, 4>  { using type = uint32_t; };
 
 template <typename T, int VX> struct Unpack;
 template <int VX> struct Unpack<uint16_t, VX> {
-  template <typename V> __device__ __forceinline__ static void run(const V& d, uint32_t* v, int32_t, uint32_t) {
+  template <typename V> __device__ __forceinline__ static void run(const V& d, uint32_t* v, int32_t, uint32_t one16) {
     const uint32_t* w = reinterpret_cast<const uint32_t*>(&d);
     #pragma unroll
-    for (int i = 0; i < VX / 2; ++i) { v[2 * i] = w[i] & 0xFFFFu; v[2 * i + 1] = w[i] >> 16; }
+    for (int i = 0; i < VX / 2; ++i) {
+      v[2 * i + 1] = w[i] >> 16;
+      v[2 * i] = DPM_UNPACK_MIX ? ptx::mad_u32(v[2 * i + 1], 0u - one16, w[i]) : (w[i] & 0xFFFFu);
+    }
   }
 };
 template <int VX> struct Unpack<int16_t, VX> {
@@ -111,6 +134,26 @@ __device__ __forceinline__ void fold_pair(uint32_t* win, const uint32_t* a, cons
     if (ha && hb) win[c] += a[ka] + b[kb];
     else if (ha) win[c] += a[ka];
     else if (hb) win[c] += b[kb];
+  }
+}
+
+// fold_pair with single adds on the FMA pipe (IMAD by a run-time 1)
+template <int NW, int VX>
+__device__ __forceinline__ void fold_pair_fma(uint32_t* win, const uint32_t* a, const uint32_t* b, int OA, int OB,
+                                              uint32_t one);
+template <int BIT, int NW, int VX>
+__device__ __forceinline__ void fold(uint32_t* win, const uint32_t* a, const uint32_t* b, int OA, int OB, uint32_t one) {
+  if constexpr (((DPM_FMA_FOLDS >> BIT) & 1) != 0) fold_pair_fma<NW, VX>(win, a, b, OA, OB, one);
+  else fold_pair<NW, VX>(win, a, b, OA, OB);
+}
+template <int NW, int VX>
+__device__ __forceinline__ void fold_pair_fma(uint32_t* win, const uint32_t* a, const uint32_t* b, int OA, int OB,
+                                              uint32_t one) {
+  #pragma unroll
+  for (int c = 0; c < NW; ++c) {
+    const int ka = c - OA, kb = c - OB;
+    if (ka >= 0 && ka < VX) win[c] = ptx::mad_u32(a[ka], one, win[c]);
+    if (kb >= 0 && kb < VX) win[c] = ptx::mad_u32(b[kb], one, win[c]);
   }
 }
 
@@ -195,6 +238,12 @@ template <int NI, int NW, int VX> struct Geo {
   // YZ plane sums staged per 8 consecutive y in shared memory (orders <= 5; at
   // order 6 the extra code costs more than the scattered atomics it saves)
   static constexpr int YZT = NI <= 6 ? SZ * 8 : 0;
+  // profile mode: the CTA's profile row (x + t z over the SX x SZ tile), in the
+  // same transposed layout (cell i at (i % VX) * SPQ + i / VX)
+  static constexpr int AQ = ProfT<NI>::value < 0 ? -ProfT<NI>::value : ProfT<NI>::value;
+  static constexpr int WQC = SX + AQ * (SZ - 1);
+  static constexpr int SPQ = (WQC + VX - 1) / VX;
+  static constexpr int PW = VX * SPQ;
 };
 
 struct ColGeom {
@@ -262,19 +311,23 @@ struct RegionCol {
   }
 };
 
-template <typename T, int NI, int NW, int VX, int STAGES>
+template <typename T, int NI, int NW, int VX, int STAGES, bool PROF>
 __global__ void __launch_bounds__(32 * NW, 1)
 project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
   using G = Geo<NI, NW, VX>;
   using V = typename Vec<T, VX>::type;
   constexpr int SX = G::SX, SZ = G::SZ, THREADS = G::THREADS;
   constexpr int N1 = VX + 7, N2 = VX + 14;             // oblique window widths
-  constexpr bool TWO_PASS = NI >= 6 && VX == 8 && NW > 8;   // +-2z images in a second pass over the stage
+#ifndef DPM_PROF_TWO_PASS
+#define DPM_PROF_TWO_PASS 0
+#endif
+  // +-2z images in a second pass over the stage (the ZX registers leave no room
+  // for them in the first); the profile mode frees those registers
+  constexpr bool TWO_PASS = NI >= 6 && VX == 8 && NW > 8 && (!PROF || DPM_PROF_TWO_PASS);
+  constexpr int TQ = ProfT<NI>::value, AQ = TQ < 0 ? -TQ : TQ;
+  constexpr int NQ = PROF ? VX + 7 * AQ : 1;           // profile window width
   constexpr uint32_t STAGE_BYTES = SX * SZ * sizeof(T);
   constexpr int YZT = G::YZT;   // words of one YZ tile (0: YZ goes straight to global)
-  // TMA producer: lane 0 of a middle warp.  The row flushes start at thread 0,
-  // so warps 0-3 carry them; keeping the producer's per-row-step work off those
-  // warps shortens the slowest warp (cfg5 -5.7 %, tools/EXPERIMENTS.md v14)
   // TMA producer: lane 0 of a middle warp.  The row flushes start at thread 0,
   // so warps 0-3 carry them; keeping the producer's per-row-step work off those
   // warps shortens the slowest warp (cfg5 -5.7 %, tools/EXPERIMENTS.md v14)
@@ -288,6 +341,11 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
   const uint32_t rows_addr = ptx::smem_addr(rows), full_addr = ptx::smem_addr(full);
 
   for (int i = tid; i < 2 * G::WORDS + 2 * YZT; i += THREADS) rows[i] = 0;
+  if constexpr (PROF) {
+    uint32_t* pr = reinterpret_cast<uint32_t*>(smem + STAGES * STAGE_BYTES + (2 * G::WORDS + 2 * YZT) * 4 +
+                                               STAGES * 8 + 64 + 160);
+    for (int i = tid; i < G::PW; i += THREADS) pr[i] = 0;
+  }
   if (tid == 0) {
     ptx::prefetch_tmap(&tmap);
     for (int i = 0; i < STAGES; ++i) ptx::mbar_init(&full[i], 1);
@@ -336,8 +394,11 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
 
   Cursor cur;
   cur.init(p);
-  uint32_t zx[8][VX];
-  int32_t col = -1;
+  uint32_t zx[8][PROF ? 1 : VX];
+  uint32_t wq[NQ];                // profile window (x + TQ z over this lane's patch), summed over y
+  #pragma unroll
+  for (int i = 0; i < NQ; ++i) wq[i] = 0;
+  int32_t col = -1, band_y0 = -1;
   ColGeom g;
   g.X0 = g.Z0 = 0; g.b = 0; g.zc = 0; g.xok = false;
   uint32_t* zx_col = nullptr;
@@ -346,6 +407,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
   // lives in shared memory (two slots by column parity: thread 0 fills the
   // next column's slot while others may still flush the previous column)
   RegionCol* rcs = reinterpret_cast<RegionCol*>(reinterpret_cast<uint8_t*>(full + STAGES) + 64);
+  uint32_t* prow = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(full + STAGES) + 64 + 160);   // [G::PW]
   int rslot = 0;
   int cst = 0, parity = 0, yzpar = 0;
   uint32_t cphase = 0;
@@ -356,6 +418,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
   // the 8 x's of its group: every red.global then covers 4 runs of 8
   // consecutive z (32 B each) instead of 32 scattered words.
   auto flush_zx = [&]() {
+    if constexpr (!PROF) {
     if (col < 0) return;
     const int j = lane & 7, g8 = lane >> 3;
     uint32_t* base = p.s.img[DPM_IMG_ZX] + (int64_t)g.b * p.L * p.N + (g.X0 + VX * 8 * g8) * p.N + g.Z0 + 8 * w + j;
@@ -381,17 +444,54 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
       for (int i = 0; i < 8; ++i)   // r[i] = plane j of x = xg + VX*i + k
         ptx::red_global_add_if(base + (int64_t)(VX * i + k) * p.N, r[i], r[i] != 0 && zok && xg + VX * i + k < p.L);
     }
+    }
+  };
+
+  // profile flush (per column and y-band, CTA-uniform): every lane adds its
+  // window to the CTA's profile row (cell VX*lane + 8*w*TQ + c, or with
+  // 8*(NW-1-w)*|TQ| for TQ < 0; transposed, so conflict-free), then the CTA
+  // adds the row to the global profile with one coalesced pass of 64-bit
+  // atomics (row cell 0 = global index X0 + TQ Z0, or X0 - |TQ|(Z0 + SZ - 1) + qoff).
+  // Only real voxels contribute, so every non-zero cell lies inside [0, WQ).
+  auto flush_prof = [&]() {
+    if constexpr (PROF) {
+      if (col < 0) return;
+      const uint32_t pa = ptx::smem_addr(prow) + 4u * lane;
+      const int lb = TQ > 0 ? 8 * w * TQ : 8 * (NW - 1 - w) * AQ;   // warp's first row cell - VX*lane
+      #pragma unroll
+      for (int c = 0; c < NQ; ++c) {
+        const int i = lb + c;   // + VX * lane
+        if (wq[c] != 0) ptx::red_shared_add_dyn(pa + 4u * ((i % VX) * G::SPQ + i / VX), wq[c]);
+        wq[c] = 0;
+      }
+      __syncthreads();
+      unsigned long long* gq = p.prof + (int64_t)g.b * p.WQ +
+                               (TQ > 0 ? g.X0 + TQ * g.Z0 : g.X0 - AQ * (g.Z0 + SZ - 1) + p.qoff);
+      for (int i = tid; i < G::WQC; i += THREADS) {
+        uint32_t* cell = prow + (i % VX) * G::SPQ + i / VX;
+        const uint32_t v = *cell;
+        *cell = 0;
+        if (v) atomicAdd(gq + i, (unsigned long long)v);
+      }
+      __syncthreads();
+    }
   };
 
   while (!cur.done) {
+    if (PROF && (cur.c != col || cur.y0 != band_y0)) {   // per column and y-band: <= 4096 rows per window sum
+      flush_prof();
+      band_y0 = cur.y0;
+    }
     if (cur.c != col) {
       flush_zx();
       col = cur.c;
       g.set(p, col, SX, SZ, VX, w, lane);
-      #pragma unroll
-      for (int t = 0; t < 8; ++t) {
+      if constexpr (!PROF) {
         #pragma unroll
-        for (int k = 0; k < VX; ++k) zx[t][k] = 0;
+        for (int t = 0; t < 8; ++t) {
+          #pragma unroll
+          for (int k = 0; k < VX; ++k) zx[t][k] = 0;
+        }
       }
       zx_col = p.s.img[DPM_IMG_ZX] + (int64_t)g.b * p.L * p.N + (g.X0 + VX * lane) * p.N + g.Z0 + 8 * w;
       yz_col = p.s.img[DPM_IMG_YZ] + (int64_t)g.b * p.M * p.N + (g.Z0 + 8 * w + (lane & 7)) * p.M;
@@ -441,19 +541,25 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
       }
       #pragma unroll
       for (int k = 0; k < VX; ++k) {
-        zx[t0][k] = ptx::mad_u32(a[k], p.one, zx[t0][k]);
-        zx[t1][k] = ptx::mad_u32(bb[k], p.one, zx[t1][k]);
+        if constexpr (!PROF) {
+          zx[t0][k] = ptx::mad_u32(a[k], p.one, zx[t0][k]);
+          zx[t1][k] = ptx::mad_u32(bb[k], p.one, zx[t1][k]);
+        }
         cs[k] += a[k] + bb[k];
+      }
+      if constexpr (PROF) {   // profile x + TQ z: window cell k + TQ t (TQ > 0) or k + |TQ| (7 - t)
+        if (TQ > 0) fold<4, NQ, VX>(wq, a, bb, TQ * t0, TQ * t1, p.one);
+        else fold<4, NQ, VX>(wq, a, bb, AQ * (7 - t0), AQ * (7 - t1), p.one);
       }
       {   // YZ: warp-wide redux of the plane sums (one REDUX per plane)
         const uint32_t s0 = __reduce_add_sync(0xffffffffu, sumv<VX>(a));
         const uint32_t s1 = __reduce_add_sync(0xffffffffu, sumv<VX>(bb));
         yzmine = lane == t0 ? s0 : (lane == t1 ? s1 : yzmine);
       }
-      fold_pair<N1, VX>(wd, a, bb, t0, t0 + 1);
-      if (NI > DPM_IMG_ANTI) fold_pair<N1, VX>(wa, a, bb, 7 - t0, 6 - t0);
-      if (!TWO_PASS && NI > DPM_IMG_X2P) fold_pair<N2, VX>(wp, a, bb, 2 * t0, 2 * t0 + 2);
-      if (!TWO_PASS && NI > DPM_IMG_X2M) fold_pair<N2, VX>(wm, a, bb, 14 - 2 * t0, 12 - 2 * t0);
+      fold<0, N1, VX>(wd, a, bb, t0, t0 + 1, p.one);
+      if (NI > DPM_IMG_ANTI) fold<1, N1, VX>(wa, a, bb, 7 - t0, 6 - t0, p.one);
+      if (!TWO_PASS && NI > DPM_IMG_X2P) fold<2, N2, VX>(wp, a, bb, 2 * t0, 2 * t0 + 2, p.one);
+      if (!TWO_PASS && NI > DPM_IMG_X2M) fold<3, N2, VX>(wm, a, bb, 14 - 2 * t0, 12 - 2 * t0, p.one);
     }
 
     // ---- YZ: lane t < 8 holds plane t of this warp (reduced in the fold loop)
@@ -491,8 +597,8 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
             #pragma unroll
             for (int k = 0; k < VX; ++k) { a[k] = ok0 ? a[k] : 0u; bb[k] = ok1 ? bb[k] : 0u; }
           }
-          fold_pair<N2, VX>(wp, a, bb, 2 * t0, 2 * t0 + 2);
-          fold_pair<N2, VX>(wm, a, bb, 14 - 2 * t0, 12 - 2 * t0);
+          fold<2, N2, VX>(wp, a, bb, 2 * t0, 2 * t0 + 2, p.one);
+          fold<3, N2, VX>(wm, a, bb, 14 - 2 * t0, 12 - 2 * t0, p.one);
         }
       }
       if (NI > DPM_IMG_X2P) {
@@ -551,6 +657,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     cur.advance_by(p, y_end - y_first);
   }
   flush_zx();
+  flush_prof();
 }
 
 // ---------------------------------------------------------------------------
@@ -592,20 +699,22 @@ template <int NI, int VX> struct WarpsFor {
   static constexpr int value = (VX == 4 && NI == 4) ? 16 : 12;
 };
 // stages: as many 4-D boxes as fit next to the row buffers
-template <typename T, int NI, int VX> struct StagesFor {
+template <typename T, int NI, int VX, bool PROF> struct StagesFor {
   static constexpr int NW = WarpsFor<NI, VX>::value;
   static constexpr int BOX = 32 * VX * 8 * NW * (int)sizeof(T);
-  static constexpr int ROWS = 2 * Geo<NI, NW, VX>::WORDS * 4 + 2 * Geo<NI, NW, VX>::YZT * 4;
+  static constexpr int ROWS = 2 * Geo<NI, NW, VX>::WORDS * 4 + 2 * Geo<NI, NW, VX>::YZT * 4 +
+                              (PROF ? Geo<NI, NW, VX>::PW * 4 : 0);
   static constexpr int FIT = (220 * 1024 - ROWS) / BOX;
   static constexpr int value = FIT > 12 ? 12 : FIT;
 };
 
-template <typename T, int NI, int VX>
+template <typename T, int NI, int VX, bool PROF>
 static int launch_one(const dpm_volume_desc* d, const void* vox, int grid, cudaStream_t st, StreamParams p) {
   constexpr int NW = WarpsFor<NI, VX>::value;
-  constexpr int S = StagesFor<T, NI, VX>::value;
+  constexpr int S = StagesFor<T, NI, VX, PROF>::value;
   using G = Geo<NI, NW, VX>;
-  constexpr size_t bytes = (size_t)S * G::SX * G::SZ * sizeof(T) + 2 * G::WORDS * 4 + 2 * G::YZT * 4 + S * 8 + 64 + 160;
+  constexpr size_t bytes = (size_t)S * G::SX * G::SZ * sizeof(T) + 2 * G::WORDS * 4 + 2 * G::YZT * 4 + S * 8 + 64 + 160 +
+                           (PROF ? G::PW * 4 : 0);
   static_assert(bytes <= 227 * 1024, "shared memory budget");
   const int64_t es = sizeof(T);
   CUtensorMap map;
@@ -619,34 +728,52 @@ static int launch_one(const dpm_volume_desc* d, const void* vox, int grid, cudaS
                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return -1;  // not describable by TMA: generic path
+  if (PROF) {   // CTA profile row cells (u32) sum <= SZ voxels per row-step: bound the rows per flush
+    const int64_t vmax = sizeof(T) == 1 ? 255 : 65535;
+    p.band = imax64(1, imin64(p.band, (int64_t)0xFFFFFFFFll / (G::SZ * vmax)));
+  }
   p.ntx = (d->L + G::SX - 1) / G::SX;
   p.ntz = (d->N + G::SZ - 1) / G::SZ;
   p.ncol = p.ntx * p.ntz * d->B;
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(project_stream_kernel<T, NI, NW, VX, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(project_stream_kernel<T, NI, NW, VX, S, PROF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)bytes);
   });
-  project_stream_kernel<T, NI, NW, VX, S><<<(int)imin64(grid, p.ncol * d->M), 32 * NW, bytes, st>>>(map, p);
+  project_stream_kernel<T, NI, NW, VX, S, PROF><<<(int)imin64(grid, p.ncol * d->M), 32 * NW, bytes, st>>>(map, p);
   return DPM_OK;
 }
 
-template <typename T, int VX>
+template <typename T, int VX, bool PROF>
 static int launch_typed(int n_img, const dpm_volume_desc* d, const void* vox, int grid, cudaStream_t st,
                         const StreamParams& p) {
   switch (n_img) {
-    case 4: return launch_one<T, 4, VX>(d, vox, grid, st, p);
-    case 5: return launch_one<T, 5, VX>(d, vox, grid, st, p);
-    case 6: return launch_one<T, 6, VX>(d, vox, grid, st, p);
-    default: return launch_one<T, 7, VX>(d, vox, grid, st, p);
+    case 4: return launch_one<T, 4, VX, PROF>(d, vox, grid, st, p);
+    case 5: return launch_one<T, 5, VX, PROF>(d, vox, grid, st, p);
+    case 6: return launch_one<T, 6, VX, PROF>(d, vox, grid, st, p);
+    default: return launch_one<T, 7, VX, PROF>(d, vox, grid, st, p);
   }
 }
 
 template <typename T>
-static int launch_vx(int n_img, const dpm_volume_desc* d, const void* vox, int grid, cudaStream_t st, const StreamParams& p) {
-  return lane_width(d) == 8 ? launch_typed<T, 8>(n_img, d, vox, grid, st, p) : launch_typed<T, 4>(n_img, d, vox, grid, st, p);
+static int launch_vx(int n_img, const dpm_volume_desc* d, const void* vox, int grid, cudaStream_t st,
+                     const StreamParams& p) {
+  if (p.prof)
+    return lane_width(d) == 8 ? launch_typed<T, 8, true>(n_img, d, vox, grid, st, p)
+                              : launch_typed<T, 4, true>(n_img, d, vox, grid, st, p);
+  return lane_width(d) == 8 ? launch_typed<T, 8, false>(n_img, d, vox, grid, st, p)
+                            : launch_typed<T, 4, false>(n_img, d, vox, grid, st, p);
 }
 
-int launch_project_stream(const dpm_volume_desc* d, const void* vox, const ImageSet& s, void*, size_t,
+int profile_shift(int n_img) {
+  return n_img <= 4 ? ProfT<4>::value : n_img == 5 ? ProfT<5>::value : n_img == 6 ? ProfT<6>::value : ProfT<7>::value;
+}
+
+bool project_stream_eligible(const dpm_volume_desc* d, const void* vox) { return stream_eligible(d, vox); }
+
+// prof != nullptr: moments mode (images except ZX + the profile along x + t z
+// summed over y, t = profile_shift(n_img)); the caller zeroed images and profile
+int launch_project_stream(const dpm_volume_desc* d, const void* vox, const ImageSet& s, unsigned long long* prof,
                           cudaStream_t st, bool* handled) {
   *handled = false;
   if (s.n_img < 4 || !stream_eligible(d, vox)) return DPM_OK;
@@ -655,12 +782,19 @@ int launch_project_stream(const dpm_volume_desc* d, const void* vox, const Image
   p.ntx = p.ntz = p.ncol = 0;  // set per lane width / warp count in launch_one
   p.one = 1;
   p.s = s;
+  p.prof = prof;
+  {
+    const int t = profile_shift(s.n_img), at = t < 0 ? -t : t;
+    p.WQ = d->L + at * (d->N - 1);
+    p.qoff = t < 0 ? at * (d->N - 1) : 0;
+  }
   // y-band: keep one band's image rows (plus the YZ cells) within ~40 MB of L2
   int64_t row_bytes = 0;
   for (int k = 0; k < s.n_img; ++k)
     if (k != DPM_IMG_YZ && k != DPM_IMG_ZX) row_bytes += s.W[k] * 4 * d->B;
   row_bytes += d->N * 4 * d->B;
   p.band = imax64(16, imin64(d->M, (40ll << 20) / imax64(row_bytes, 1)));
+
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

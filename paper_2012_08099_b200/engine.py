@@ -196,20 +196,83 @@ def moments2d_images(vox: torch.Tensor, imgs: list[torch.Tensor], order: int, of
     return acc
 
 
+def profile_layout(desc: nat.VolumeDesc, order: int) -> tuple[int, int, int]:
+    """(WQ, ai, t) of the moments pipeline's y-summed profile P[x + t z]."""
+    wq, ai, t = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
+    nat.check(nat.lib().dpm_profile_layout(ctypes.byref(desc), order, ctypes.byref(wq), ctypes.byref(ai),
+                                           ctypes.byref(t)), "dpm_profile_layout")
+    return int(wq.value), int(ai.value), int(t.value)
+
+
 def moments2d_partial(vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0,
-                      stream: torch.cuda.Stream | None = None) -> torch.Tensor:
-    """Project + exact 2D moments of a slab in GLOBAL coordinates; returns the
-    limb accumulator [B, n_img, n2d, 4].  Limb accumulators of z-slabs add
-    elementwise (moments are linear in the voxels)."""
+                      stream: torch.cuda.Stream | None = None, acc: torch.Tensor | None = None,
+                      workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """The moments pipeline's projection pass + exact moments of a slab in
+    GLOBAL coordinates (dpm_moments_partial); returns the DPM_ACC_PROFILE limb
+    accumulator [B, n_img, n2d, 4].  Accumulators of z-slabs add elementwise
+    (moments are linear in the voxels); finish with ``derive(acc, order)``."""
     check_order(order)
-    imgs = project(vox, num_images(order), offset, z0, stream)
-    return moments2d_images(vox, imgs, order, offset, z0, stream)
+    desc = make_desc(vox, offset, z0)
+    lib = nat.lib()
+    wsb = int(lib.dpm_partial_workspace_bytes(ctypes.byref(desc), order))
+    if wsb == 0:
+        raise ValueError("invalid volume descriptor")
+    ws = workspace if workspace is not None else _WS.get(wsb, vox.device)
+    if acc is None:
+        acc = torch.empty((desc.B, num_images(order), n2d(order), 4), dtype=torch.int64, device=vox.device)
+    nat.check(lib.dpm_moments_partial(ctypes.byref(desc), vox.data_ptr(), order, ws.data_ptr(), wsb,
+                                      acc.data_ptr(), stream_handle(stream)), "dpm_moments_partial")
+    return acc
+
+
+def project_profile(vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0,
+                    stream: torch.cuda.Stream | None = None, imgs: list[torch.Tensor | None] | None = None,
+                    profile: torch.Tensor | None = None) -> tuple[list[torch.Tensor | None], torch.Tensor]:
+    """Projection pass of the moments pipeline: the order's images except ZX
+    (slot 2 is None) as int32 [B, H, W] uint32 bits, and the y-summed profile
+    as int64 [B, WQ] (uint64 bits)."""
+    check_order(order)
+    desc = make_desc(vox, offset, z0)
+    n_img = num_images(order)
+    if imgs is None:
+        imgs = []
+        for k in range(n_img):
+            W, H, _, _ = image_layout(desc, k)
+            imgs.append(None if k == 2 else torch.empty((desc.B, H, W), dtype=torch.int32, device=vox.device))
+    if profile is None:
+        wq, _, _ = profile_layout(desc, order)
+        profile = torch.empty((desc.B, wq), dtype=torch.int64, device=vox.device)
+    ptrs = (ctypes.c_void_p * n_img)(*[t.data_ptr() if t is not None else None for t in imgs])
+    nat.check(nat.lib().dpm_project_profile(ctypes.byref(desc), vox.data_ptr(), order, ptrs, profile.data_ptr(),
+                                            stream_handle(stream)), "dpm_project_profile")
+    return imgs, profile
+
+
+def moments2d_profile(vox: torch.Tensor, imgs: list[torch.Tensor | None], profile: torch.Tensor, order: int,
+                      offset: int = 0, z0: int = 0, stream: torch.cuda.Stream | None = None,
+                      acc: torch.Tensor | None = None) -> torch.Tensor:
+    """DPM_ACC_PROFILE accumulator of ``project_profile`` outputs."""
+    desc = make_desc(vox, offset, z0)
+    n_img = len(imgs)
+    if acc is None:
+        acc = torch.empty((desc.B, n_img, n2d(order), 4), dtype=torch.int64, device=vox.device)
+    ptrs = (ctypes.c_void_p * n_img)(*[t.data_ptr() if t is not None else None for t in imgs])
+    nat.check(nat.lib().dpm_moments2d_profile(ctypes.byref(desc), order, ptrs, profile.data_ptr(), acc.data_ptr(),
+                                              stream_handle(stream)), "dpm_moments2d_profile")
+    return acc
+
+
+ACC_KINDS = {"profile": nat.DPM_ACC_PROFILE, "images": nat.DPM_ACC_IMAGES}
 
 
 def derive(acc: torch.Tensor, order: int, stream: torch.cuda.Stream | None = None,
-           out: DeviceMoments | None = None) -> DeviceMoments:
-    """Device epilogue on a (possibly summed) limb accumulator."""
+           out: DeviceMoments | None = None, kind: str = "profile") -> DeviceMoments:
+    """Device epilogue on a (possibly summed) limb accumulator: ``kind``
+    "profile" for ``moments2d_partial`` / ``moments2d_profile`` accumulators,
+    "images" for ``moments2d_images`` over ``project``'s image set."""
     check_order(order)
+    if kind not in ACC_KINDS:
+        raise ValueError(f"unknown accumulator kind {kind!r}")
     B = acc.shape[0]
     desc = nat.VolumeDesc()
     desc.L = desc.M = desc.N = 1
@@ -220,7 +283,7 @@ def derive(acc: torch.Tensor, order: int, stream: torch.cuda.Stream | None = Non
             i128=torch.empty((B, n3d(order), 2), dtype=torch.int64, device=dev),
             f64=torch.empty((B, n3d(order)), dtype=torch.float64, device=dev),
             status=torch.empty((B,), dtype=torch.int32, device=dev), launches=0)
-    nat.check(nat.lib().dpm_derive3d(ctypes.byref(desc), acc.data_ptr(), order, out.i128.data_ptr(),
+    nat.check(nat.lib().dpm_derive3d(ctypes.byref(desc), acc.data_ptr(), order, ACC_KINDS[kind], out.i128.data_ptr(),
                                      out.f64.data_ptr(), out.status.data_ptr(), stream_handle(stream)),
               "dpm_derive3d")
     out.launches = nat.last_launch_count()
@@ -302,8 +365,9 @@ class GraphedMoments:
 
 class GraphedSlabStages:
     """The z-slab pipeline as three CUDA graphs over fixed buffers: (1) the
-    projection (image zeroing + streaming pass), (2) exact 2D moments in
-    global coordinates into ``acc``, (3) the epilogue into ``out``.  A
+    projection (image/profile zeroing + streaming pass, ``project_profile``),
+    (2) exact 2D/1D moments in global coordinates into ``acc``, (3) the
+    epilogue into ``out``.  A
     multi-GPU caller all-reduces ``acc`` between (2) and (3) (the exchange is
     not captured).  Replays are issued on the caller's current stream."""
 
@@ -316,9 +380,9 @@ class GraphedSlabStages:
         self.imgs = []
         for k in range(n_img):
             W, H, _, _ = image_layout(desc, k)
-            self.imgs.append(torch.empty((desc.B, H, W), dtype=torch.int32, device=dev))
-        wsb = int(nat.lib().dpm_project_workspace_bytes(ctypes.byref(desc), n_img))
-        self.ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device=dev) if wsb else None
+            self.imgs.append(None if k == 2 else torch.empty((desc.B, H, W), dtype=torch.int32, device=dev))
+        wq, _, _ = profile_layout(desc, order)
+        self.profile = torch.empty((desc.B, wq), dtype=torch.int64, device=dev)
         self.acc = torch.empty((desc.B, n_img, n2d(order), 4), dtype=torch.int64, device=dev)
         self.out = DeviceMoments(
             i128=torch.empty((desc.B, n3d(order), 2), dtype=torch.int64, device=dev),
@@ -340,10 +404,10 @@ class GraphedSlabStages:
         torch.cuda.current_stream(dev).wait_stream(st)
 
     def _project(self):
-        project(self.vox, len(self.imgs), self.offset, self.z0, imgs=self.imgs, workspace=self.ws)
+        project_profile(self.vox, self.order, self.offset, self.z0, imgs=self.imgs, profile=self.profile)
 
     def _moments2d(self):
-        moments2d_images(self.vox, self.imgs, self.order, self.offset, self.z0, acc=self.acc)
+        moments2d_profile(self.vox, self.imgs, self.profile, self.order, self.offset, self.z0, acc=self.acc)
 
     def _derive(self):
         derive(self.acc, self.order, out=self.out)

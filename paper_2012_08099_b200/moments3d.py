@@ -165,12 +165,14 @@ def dpm_moments_batch(volumes, order: int, check_consistency: bool = True, offse
 
 def dpm_generic_moments(volume: Volume, order: int, counters: OpCounters | None = None,
                         check_consistency: bool = True) -> MomentTensor3:
-    """The DPM pipeline with the projection pass forced through the shape-generic
-    brick kernel (``dpm_project_generic``) instead of the TMA streaming kernel;
-    2D moments and epilogue as in ``dpm_moments``.  A second, independently
-    written device projection engine, so ``harness.verify_engines`` cross-checks
-    two implementations the way the reference cross-checks its engines
-    (moments3d.py:267-271, harness.py:101-120)."""
+    """A second, independent device route: the reference's image set (with the
+    ZX image, no profile) built by the shape-generic brick kernel
+    (``dpm_project_generic``) instead of the TMA streaming kernel, its 2D
+    moments, and the epilogue placing M_{p,0,r} from ZX.  ``dpm_moments`` uses
+    a different kernel AND a different set of projections (profile instead of
+    ZX), so ``harness.verify_engines`` cross-checks two implementations the way
+    the reference cross-checks its engines (moments3d.py:267-271,
+    harness.py:101-120)."""
     import torch
 
     from . import engine
@@ -183,7 +185,7 @@ def dpm_generic_moments(volume: Volume, order: int, counters: OpCounters | None 
                           order)
     imgs = engine.project(vox, engine.num_images(order), kernel="generic")
     acc = engine.moments2d_images(vox, imgs, order)
-    res = engine.derive(acc, order)
+    res = engine.derive(acc, order, kind="images")
     torch.cuda.current_stream().synchronize()
     st = int(res.status[0].item())
     if check_consistency:

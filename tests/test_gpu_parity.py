@@ -137,7 +137,7 @@ def test_inconsistency_detected_on_corrupted_image(cuda):
     imgs = engine.project(v, 5)
     imgs[0][0, 0, 0] += 1
     acc = engine.moments2d_images(v, imgs, 4)
-    res = engine.derive(acc, 4)
+    res = engine.derive(acc, 4, kind="images")
     torch.cuda.synchronize()
     from paper_2012_08099_b200.moments3d import raise_status
     with pytest.raises(InconsistencyError, match="disagree"):

@@ -1,0 +1,114 @@
+"""The moments pipeline's projection set: the order's
+images without ZX plus the y-summed profile P[x + t z].  Images must be
+bit-identical to ``project``'s, the profile to a numpy restatement, and the
+moments to the oracle and to the independent images route (``dpm_generic``)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2012_08099_b200 as vm
+from paper_2012_08099_b200 import engine
+
+pytestmark = pytest.mark.gpu
+
+T_OF_ORDER = {3: -1, 4: 2, 5: -2, 6: 3}
+
+
+def np_profile(vol: np.ndarray, t: int) -> np.ndarray:
+    """P[x + t z (+ |t|(N-1) if t < 0)] = sum_y V[z, y, x] (test restatement)."""
+    n, m, l = vol.shape
+    at = abs(t)
+    out = np.zeros(l + at * (n - 1), dtype=np.int64)
+    cols = vol.astype(np.int64).sum(axis=1)          # [z, x]
+    x = np.arange(l)
+    for z in range(n):
+        idx = x + t * z + (at * (n - 1) if t < 0 else 0)
+        np.add.at(out, idx, cols[z])
+    return out
+
+
+def _ints(res):
+    return [engine.i128_to_ints(res.i128[b].cpu().numpy()) for b in range(res.i128.shape[0])]
+
+
+SHAPES = [
+    ((24, 40, 264), np.uint16),     # TMA streaming kernel, VX = 8, partial x-tile
+    ((100, 17, 256), np.uint16),    # two z-tiles
+    ((16, 8, 64), np.uint8),        # VX = 4
+    ((9, 7, 5), np.uint8),          # generic kernel
+    ((13, 11, 203), np.uint16),     # generic kernel (unaligned rows)
+]
+
+
+@pytest.mark.parametrize("order", [3, 4, 5, 6])
+@pytest.mark.parametrize("shape,dt", SHAPES)
+def test_profile_images_and_profile(order, shape, dt):
+    rng = np.random.default_rng(sum(shape) + order)
+    vol = rng.integers(0, np.iinfo(dt).max + 1, size=shape).astype(dt)
+    v = torch.from_numpy(vol).cuda()
+    imgs, prof = engine.project_profile(v, order)
+    ref = engine.project(v, engine.num_images(order))
+    torch.cuda.synchronize()
+    assert imgs[2] is None
+    for k in range(engine.num_images(order)):
+        if k != 2:
+            assert torch.equal(imgs[k], ref[k]), k
+    wq, ai, t = engine.profile_layout(engine.make_desc(v), order)
+    assert t == T_OF_ORDER[order] and wq == shape[2] + abs(t) * (shape[0] - 1)
+    assert ai == (-abs(t) * (shape[0] - 1) if t < 0 else 0)
+    assert np.array_equal(prof[0].cpu().numpy(), np_profile(vol, t))
+
+
+@pytest.mark.parametrize("order", [3, 4, 5, 6])
+@pytest.mark.parametrize("shape,dt", SHAPES + [((40, 1500, 256), np.uint16)])   # tall: several y-bands per column
+def test_profile_moments_match_oracle_and_images_route(order, shape, dt):
+    rng = np.random.default_rng(7 * order + shape[0])
+    vol = rng.integers(0, np.iinfo(dt).max + 1, size=shape).astype(dt)
+    v = vm.Volume(vol)
+    got = vm.dpm_moments(v, order)
+    assert got.values == vm.dpm_generic_moments(v, order).values
+    if np.prod(shape) <= 200_000:
+        assert got.values == oracle.naive(vol, order)
+
+
+@pytest.mark.parametrize("order", [3, 6])
+def test_profile_zslab_composition(order):
+    rng = np.random.default_rng(11)
+    vol = rng.integers(0, 65536, size=(70, 20, 256)).astype(np.uint16)
+    whole = _ints(engine.derive(engine.moments2d_partial(torch.from_numpy(vol).cuda(), order), order))
+    for cuts in ([0, 33, 70], [0, 5, 6, 40, 70]):
+        acc = None
+        for z0, z1 in zip(cuts[:-1], cuts[1:]):
+            part = engine.moments2d_partial(torch.from_numpy(vol[z0:z1]).cuda(), order, z0=z0)
+            acc = part.clone() if acc is None else acc + part
+        assert _ints(engine.derive(acc, order)) == whole
+
+
+def test_profile_batch_and_offset():
+    rng = np.random.default_rng(5)
+    vols = rng.integers(-1024, 3072, size=(3, 16, 12, 128)).astype(np.int16)
+    got = vm.dpm_moments_batch(vols, 4, offset=1024)
+    for b in range(3):
+        want = oracle.naive((vols[b].astype(np.int32) + 1024).astype(np.uint16), 4)
+        assert got[b].values == want
+
+
+@pytest.mark.parametrize("order,a", [(6, 3), (5, 2), (4, 1), (3, 2)])
+def test_profile_fault_injection_is_detected(order, a):
+    """A corrupted profile moment in a redundant row is caught (DPM_ST_DISAGREE)."""
+    rng = np.random.default_rng(order)
+    vol = rng.integers(0, 65536, size=(24, 16, 256)).astype(np.uint16)
+    acc = engine.moments2d_partial(torch.from_numpy(vol).cuda(), order)
+    assert int(engine.derive(acc, order).status[0]) == 0
+    bad = acc.clone()
+    p_idx = a * (order + 1) - a * (a - 1) // 2      # idx2(order, a, 0)
+    bad[0, 2, p_idx, 0] += 1
+    assert int(engine.derive(bad, order).status[0]) & 1
+
+
+def test_profile_graphed_stages_launches():
+    rng = np.random.default_rng(2)
+    slab = torch.from_numpy(rng.integers(0, 65535, size=(24, 24, 264)).astype(np.uint16)).cuda()
+    st = engine.GraphedSlabStages(slab, 6, z0=16)
+    assert st.launches == 4      # projection, image moments, profile moments, epilogue

@@ -1,4 +1,5 @@
-# A/B/C: three builds on one box
+# A/B/C: up to three builds of libdpm_b200.so on one box; ncu kernel time of
+# the projection kernel per case (MODE=profile times the moments-pipeline pass)
 cases=${CASES:-"cfg5|1024^3 u16 K4|cfg4"}
 IFS='|' read -ra CS <<< "$cases"
 for rep in 1 2; do
@@ -6,7 +7,7 @@ for rep in 1 2; do
     [ -f tools/ab/$v.so ] || continue
     cp tools/ab/$v.so paper_2012_08099_b200/libdpm_b200.so
     for c in "${CS[@]}"; do
-      t=$(ncu --metrics gpu__time_duration.sum --clock-control none -k regex:${KREGEX:-project_stream} -c 3 --csv python tools/time_project.py "$c" 2>/dev/null | grep ${KREGEX:-project_stream} | tail -1 | rev | cut -d, -f1 | rev)
+      t=$(ncu --metrics gpu__time_duration.sum --clock-control none -k regex:${KREGEX:-project_stream} -c 3 --csv python tools/time_project.py "$c" ${MODE:-} 2>/dev/null | grep ${KREGEX:-project_stream} | tail -1 | rev | cut -d, -f1 | rev)
       echo "$rep $v $c $t"
     done
   done

@@ -25,6 +25,7 @@ def timeit(fn, reps=10, warm=3):
 
 def main():
     only = sys.argv[1] if len(sys.argv) > 1 else ""
+    profile_only = len(sys.argv) > 2 and sys.argv[2] == "profile"   # (ncu A/B: time the moments-pipeline pass only)
     cases = [("cfg3-like 512^3 u16 K4", (512, 512, 512), torch.uint16, 4),
              ("cfg2 256^3 u16 K3", (256, 256, 256), torch.uint16, 3),
              ("1024^3 u16 K6", (1024, 1024, 1024), torch.uint16, 6),
@@ -45,11 +46,17 @@ def main():
         else:
             v = torch.randint(0, 256, shape, dtype=torch.uint8, device="cuda")
         nbytes = v.numel() * v.element_size()
+        if profile_only:
+            tq = timeit(lambda: engine.project_profile(v, K))
+            print(f"{name}: project_profile {tq:.3f} ms ({nbytes / tq / 1e6:.0f} GB/s)", flush=True)
+            continue
         tp = timeit(lambda: engine.project(v, engine.num_images(K)))
+        tq = timeit(lambda: engine.project_profile(v, K))
         imgs = engine.project(v, engine.num_images(K))
         t2 = timeit(lambda: engine.moments2d_images(v, imgs, K))
         tm = timeit(lambda: engine.moments(v, K))
-        print(f"{name}: project {tp:.3f} ms ({nbytes / tp / 1e6:.0f} GB/s)  moments2d {t2:.3f} ms  full {tm:.3f} ms "
+        print(f"{name}: project {tp:.3f} ms ({nbytes / tp / 1e6:.0f} GB/s)  "
+              f"project_profile {tq:.3f} ms ({nbytes / tq / 1e6:.0f} GB/s)  moments2d {t2:.3f} ms  full {tm:.3f} ms "
               f"({nbytes / tm / 1e6:.0f} GB/s, {n / tm / 1e6:.0f} GVox/s)", flush=True)
         del v
         torch.cuda.empty_cache()
