@@ -68,6 +68,10 @@ static size_t images_bytes(const dpm_volume_desc* d, int n_img, size_t* offs, bo
   return total;
 }
 
+static size_t acc_bytes_of(const dpm_volume_desc* d, int order) {
+  return align256((size_t)(d->B * num_images(order) * n2d(order) * 4) * sizeof(uint64_t));
+}
+
 // the y-summed profile of the moments pipeline: direction t, stored length WQ,
 // logical coordinate = stored index + ai (global z: ai includes t * z0)
 struct ProfGeom { int t; int64_t WQ, ai; };
@@ -161,6 +165,31 @@ int dpm_profile_layout(const dpm_volume_desc* desc, int order, int64_t* WQ, int6
   return DPM_OK;
 }
 
+// moments-pipeline projection kernel on already zeroed images + profile
+static int project_profile_launch(const dpm_volume_desc* desc, const void* d_voxels, int order,
+                                  uint32_t* const* d_images, uint64_t* d_profile, cudaStream_t st) {
+  ImageSet s = make_set(desc, num_images(order), d_images, true);
+  unsigned long long* prof = reinterpret_cast<unsigned long long*>(d_profile);
+  bool handled = false;
+  const int rc = launch_project_stream(desc, d_voxels, s, prof, st, &handled);
+  if (rc || handled) return rc;
+  return launch_project_generic(desc, d_voxels, s, prof, st);
+}
+
+// image + profile moments into an already zeroed DPM_ACC_PROFILE accumulator
+static int moments2d_profile_launch(const dpm_volume_desc* desc, int order, const uint32_t* const* d_images,
+                                    const uint64_t* d_profile, uint64_t* d_acc, cudaStream_t st) {
+  const int n_img = num_images(order);
+  ImageSet s = make_set(desc, n_img, const_cast<uint32_t* const*>(d_images), true);
+  const int jb = jbits_for(desc, n_img);
+  if (jb > 21) return DPM_EOVERFLOW;
+  int rc = launch_moments2d(s, desc->B, order, jb, d_acc, st);
+  if (rc) return rc;
+  const ProfGeom pg = profile_geom(desc, order);
+  return launch_profile_moments(reinterpret_cast<const unsigned long long*>(d_profile), pg.WQ, desc->B, pg.ai, order,
+                                n_img, DPM_IMG_ZX, d_acc, st);
+}
+
 int dpm_project_profile(const dpm_volume_desc* desc, const void* d_voxels, int order, uint32_t* const* d_images,
                         uint64_t* d_profile, void* stream) {
   reset_launches();
@@ -178,11 +207,7 @@ int dpm_project_profile(const dpm_volume_desc* desc, const void* d_voxels, int o
   }
   const ProfGeom pg = profile_geom(desc, order);
   if (cudaMemsetAsync(d_profile, 0, (size_t)(pg.WQ * desc->B) * sizeof(uint64_t), st) != cudaSuccess) return DPM_ECUDA;
-  unsigned long long* prof = reinterpret_cast<unsigned long long*>(d_profile);
-  bool handled = false;
-  rc = launch_project_stream(desc, d_voxels, s, prof, st, &handled);
-  if (rc || handled) return rc;
-  return launch_project_generic(desc, d_voxels, s, prof, st);
+  return project_profile_launch(desc, d_voxels, order, d_images, d_profile, st);
 }
 
 int dpm_moments2d_profile(const dpm_volume_desc* desc, int order, const uint32_t* const* d_images,
@@ -193,17 +218,9 @@ int dpm_moments2d_profile(const dpm_volume_desc* desc, int order, const uint32_t
   if (check_order(order) || !d_images || !d_profile || !d_acc) return DPM_EINVAL;
   const int n_img = num_images(order);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  ImageSet s = make_set(desc, n_img, const_cast<uint32_t* const*>(d_images), true);
-  const int jb = jbits_for(desc, n_img);
-  if (jb > 21) return DPM_EOVERFLOW;
   if (cudaMemsetAsync(d_acc, 0, (size_t)(desc->B * n_img * n2d(order) * 4) * sizeof(uint64_t), st) != cudaSuccess)
     return DPM_ECUDA;
-  rc = launch_moments2d(s, desc->B, order, jb, d_acc, st);
-  if (rc) return rc;
-  const ProfGeom pg = profile_geom(desc, order);
-  rc = launch_profile_moments(reinterpret_cast<const unsigned long long*>(d_profile), pg.WQ, desc->B, pg.ai, order,
-                              n_img, DPM_IMG_ZX, d_acc, st);
-  return rc;
+  return moments2d_profile_launch(desc, order, d_images, d_profile, d_acc, st);
 }
 
 size_t dpm_partial_workspace_bytes(const dpm_volume_desc* desc, int order) {
@@ -212,8 +229,10 @@ size_t dpm_partial_workspace_bytes(const dpm_volume_desc* desc, int order) {
   return images_bytes(desc, num_images(order), nullptr, true) + align256((size_t)(pg.WQ * desc->B) * sizeof(uint64_t));
 }
 
-int dpm_moments_partial(const dpm_volume_desc* desc, const void* d_voxels, int order, void* d_ws, size_t ws_bytes,
-                        uint64_t* d_acc, void* stream) {
+// acc_adjacent: d_acc is the acc_bytes_of() bytes right before d_ws (dpm_moments'
+// own workspace carve), so one memset zeroes accumulator, images and profile
+static int moments_partial_impl(const dpm_volume_desc* desc, const void* d_voxels, int order, void* d_ws,
+                                size_t ws_bytes, uint64_t* d_acc, void* stream, bool acc_adjacent) {
   int rc = check_desc(desc);
   if (rc) return rc;
   if (check_order(order) || !d_voxels || !d_acc) return DPM_EINVAL;
@@ -225,14 +244,24 @@ int dpm_moments_partial(const dpm_volume_desc* desc, const void* d_voxels, int o
   char* base = static_cast<char*>(d_ws);
   for (int k = 0; k < n_img; ++k) imgs[k] = k == DPM_IMG_ZX ? nullptr : reinterpret_cast<uint32_t*>(base + offs[k]);
   uint64_t* prof = reinterpret_cast<uint64_t*>(base + ib);
-  int launches = 0;
-  rc = dpm_project_profile(desc, d_voxels, order, imgs, prof, stream);
-  launches += dpm_last_launch_count();
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // one zeroing of the contiguous images + profile scratch, one of the accumulator
+  // (or none when the caller's accumulator directly precedes it: dpm_moments)
+  char* z0 = acc_adjacent ? reinterpret_cast<char*>(d_acc) : base;
+  const size_t zb = dpm_partial_workspace_bytes(desc, order) + (acc_adjacent ? acc_bytes_of(desc, order) : 0);
+  if (cudaMemsetAsync(z0, 0, zb, st) != cudaSuccess) return DPM_ECUDA;
+  if (!acc_adjacent &&
+      cudaMemsetAsync(d_acc, 0, (size_t)(desc->B * n_img * n2d(order) * 4) * sizeof(uint64_t), st) != cudaSuccess)
+    return DPM_ECUDA;
+  reset_launches();
+  rc = project_profile_launch(desc, d_voxels, order, imgs, prof, st);
   if (rc) return rc;
-  rc = dpm_moments2d_profile(desc, order, imgs, prof, d_acc, stream);
-  launches += dpm_last_launch_count();
-  g_launches = launches;
-  return rc;
+  return moments2d_profile_launch(desc, order, imgs, prof, d_acc, st);
+}
+
+int dpm_moments_partial(const dpm_volume_desc* desc, const void* d_voxels, int order, void* d_ws, size_t ws_bytes,
+                        uint64_t* d_acc, void* stream) {
+  return moments_partial_impl(desc, d_voxels, order, d_ws, ws_bytes, d_acc, stream, false);
 }
 
 int dpm_moments2d(const dpm_volume_desc* desc, int n_img, const uint32_t* const* d_images, int order,
@@ -307,12 +336,11 @@ int dpm_moments(const dpm_volume_desc* desc, const void* d_voxels, int order, vo
   if (rc) return rc;
   if (check_order(order) || !d_voxels || !d_m3d_i128 || !d_status) return DPM_EINVAL;
   if (ws_bytes < dpm_workspace_bytes(desc, order) || !d_ws) return DPM_EWORKSPACE;
-  const int n_img = num_images(order);
   uint64_t* acc = static_cast<uint64_t*>(d_ws);
-  const size_t acc_bytes = align256((size_t)(desc->B * n_img * n2d(order) * 4) * sizeof(uint64_t));
+  const size_t acc_bytes = acc_bytes_of(desc, order);
   int launches = 0;
-  rc = dpm_moments_partial(desc, d_voxels, order, static_cast<char*>(d_ws) + acc_bytes, ws_bytes - acc_bytes, acc,
-                           stream);
+  rc = moments_partial_impl(desc, d_voxels, order, static_cast<char*>(d_ws) + acc_bytes, ws_bytes - acc_bytes, acc,
+                            stream, true);
   launches += dpm_last_launch_count();
   if (rc) return rc;
   rc = dpm_derive3d(desc, acc, order, DPM_ACC_PROFILE, d_m3d_i128, d_m3d_f64, d_status, stream);

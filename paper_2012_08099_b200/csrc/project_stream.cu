@@ -548,8 +548,16 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
         cs[k] += a[k] + bb[k];
       }
       if constexpr (PROF) {   // profile x + TQ z: window cell k + TQ t (TQ > 0) or k + |TQ| (7 - t)
-        if (TQ > 0) fold<4, NQ, VX>(wq, a, bb, TQ * t0, TQ * t1, p.one);
-        else fold<4, NQ, VX>(wq, a, bb, AQ * (7 - t0), AQ * (7 - t1), p.one);
+        // plane pair 3 of orders <= 5 folds the profile with IADD3 (ALU), the
+        // rest with IMAD (FMA): the pipe balance measured best (EXPERIMENTS.md v24)
+        constexpr int ALU_PAIRS = NI >= 7 ? 0 : 8;
+        if (((ALU_PAIRS >> tp) & 1) != 0) {
+          if (TQ > 0) fold_pair<NQ, VX>(wq, a, bb, TQ * t0, TQ * t1);
+          else fold_pair<NQ, VX>(wq, a, bb, AQ * (7 - t0), AQ * (7 - t1));
+        } else {
+          if (TQ > 0) fold<4, NQ, VX>(wq, a, bb, TQ * t0, TQ * t1, p.one);
+          else fold<4, NQ, VX>(wq, a, bb, AQ * (7 - t0), AQ * (7 - t1), p.one);
+        }
       }
       {   // YZ: warp-wide redux of the plane sums (one REDUX per plane)
         const uint32_t s0 = __reduce_add_sync(0xffffffffu, sumv<VX>(a));
