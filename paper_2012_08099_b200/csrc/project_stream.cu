@@ -114,8 +114,29 @@ template <int VX> struct Unpack<uint8_t, VX> {
     #pragma unroll
     for (int i = 0; i < VX / 4; ++i) {
       #pragma unroll
-      for (int j = 0; j < 4; ++j) v[4 * i + j] = (w[i] >> (8 * j)) & 0xFFu;
+      for (int j = 0; j < 4; ++j) v[4 * i + j] = __byte_perm(w[i], 0u, 0x4440u + j);   // one PRMT per byte
     }
+  }
+};
+
+// Sum of a lane's VX voxels of one plane straight from the packed vector:
+// byte dot products with ones (IDP, FMA pipe), independent of the unpack, and
+// two planes per redux.  Used for 8-wide uint8 lanes only: measured faster
+// there (1024^3 u8 K3 -12 %), slower for 4-wide u8 lanes (cfg4 +3 %) and for
+// uint16 with __dp2a (cfg5 +3 %) -- tools/EXPERIMENTS.md v25.
+template <typename T, int VX> struct PlaneSum {
+  static constexpr bool packed = sizeof(T) == 1 && VX == 8;
+  template <typename V> __device__ __forceinline__ static uint32_t run(const V& d) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(&d);
+    uint32_t s = 0;
+    if constexpr (sizeof(T) == 1) {
+      #pragma unroll
+      for (int i = 0; i < VX / 4; ++i) s = __dp4a(w[i], 0x01010101u, s);
+    } else {
+      #pragma unroll
+      for (int i = 0; i < VX / 2; ++i) s = __dp2a_lo(w[i], 0x0101u, s);
+    }
+    return s;
   }
 };
 
@@ -560,9 +581,16 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
         }
       }
       {   // YZ: warp-wide redux of the plane sums (one REDUX per plane)
-        const uint32_t s0 = __reduce_add_sync(0xffffffffu, sumv<VX>(a));
-        const uint32_t s1 = __reduce_add_sync(0xffffffffu, sumv<VX>(bb));
-        yzmine = lane == t0 ? s0 : (lane == t1 ? s1 : yzmine);
+        if constexpr (PlaneSum<T, VX>::packed && sizeof(T) == 1) {
+          // u8: both plane sums in one redux (16-bit fields: 32 lanes x VX x 255 < 2^16)
+          const uint32_t r = __reduce_add_sync(0xffffffffu, ptx::mad_u32(PlaneSum<T, VX>::run(dv[t1]), p.one << 16,
+                                                                         PlaneSum<T, VX>::run(dv[t0])));
+          yzmine = lane == t0 ? (r & 0xFFFFu) : (lane == t1 ? (r >> 16) : yzmine);
+        } else {
+          const uint32_t s0 = __reduce_add_sync(0xffffffffu, PlaneSum<T, VX>::packed ? PlaneSum<T, VX>::run(dv[t0]) : sumv<VX>(a));
+          const uint32_t s1 = __reduce_add_sync(0xffffffffu, PlaneSum<T, VX>::packed ? PlaneSum<T, VX>::run(dv[t1]) : sumv<VX>(bb));
+          yzmine = lane == t0 ? s0 : (lane == t1 ? s1 : yzmine);
+        }
       }
       fold<0, N1, VX>(wd, a, bb, t0, t0 + 1, p.one);
       if (NI > DPM_IMG_ANTI) fold<1, N1, VX>(wa, a, bb, 7 - t0, 6 - t0, p.one);
