@@ -333,7 +333,10 @@ struct RegionCol {
 };
 
 template <typename T, int NI, int NW, int VX, int STAGES, bool PROF>
-__global__ void __launch_bounds__(32 * NW, 1)
+#ifndef DPM_CTAS
+#define DPM_CTAS 1   // resident CTAs per SM (the 12 / 16 warps of an SM split over them)
+#endif
+__global__ void __launch_bounds__(32 * NW, DPM_CTAS)
 project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
   using G = Geo<NI, NW, VX>;
   using V = typename Vec<T, VX>::type;
@@ -732,7 +735,7 @@ size_t project_stream_workspace(const dpm_volume_desc*, int) { return 0; }
 // of orders >= 5 need more registers (then 8 warps, <= 255 registers); the
 // 4-wide lanes of order 3 fit 128 registers, so 16 warps (128-plane z-tiles)
 template <int NI, int VX> struct WarpsFor {
-  static constexpr int value = (VX == 4 && NI == 4) ? 16 : 12;
+  static constexpr int value = ((VX == 4 && NI == 4) ? 16 : 12) / DPM_CTAS;
 };
 // stages: as many 4-D boxes as fit next to the row buffers
 template <typename T, int NI, int VX, bool PROF> struct StagesFor {
@@ -740,7 +743,7 @@ template <typename T, int NI, int VX, bool PROF> struct StagesFor {
   static constexpr int BOX = 32 * VX * 8 * NW * (int)sizeof(T);
   static constexpr int ROWS = 2 * Geo<NI, NW, VX>::WORDS * 4 + 2 * Geo<NI, NW, VX>::YZT * 4 +
                               (PROF ? Geo<NI, NW, VX>::PW * 4 : 0);
-  static constexpr int FIT = (220 * 1024 - ROWS) / BOX;
+  static constexpr int FIT = ((DPM_CTAS == 1 ? 220 : 111) * 1024 - ROWS) / BOX;
   static constexpr int value = FIT > 12 ? 12 : FIT;
 };
 
@@ -751,7 +754,7 @@ static int launch_one(const dpm_volume_desc* d, const void* vox, int grid, cudaS
   using G = Geo<NI, NW, VX>;
   constexpr size_t bytes = (size_t)S * G::SX * G::SZ * sizeof(T) + 2 * G::WORDS * 4 + 2 * G::YZT * 4 + S * 8 + 64 + 160 +
                            (PROF ? G::PW * 4 : 0);
-  static_assert(bytes <= 227 * 1024, "shared memory budget");
+  static_assert(bytes <= (DPM_CTAS == 1 ? 227 : 112) * 1024, "shared memory budget");
   const int64_t es = sizeof(T);
   CUtensorMap map;
   const cuuint64_t dims[4] = {(cuuint64_t)d->L, (cuuint64_t)d->M, (cuuint64_t)d->N, (cuuint64_t)d->B};
@@ -776,7 +779,8 @@ static int launch_one(const dpm_volume_desc* d, const void* vox, int grid, cudaS
     cudaFuncSetAttribute(project_stream_kernel<T, NI, NW, VX, S, PROF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)bytes);
   });
-  project_stream_kernel<T, NI, NW, VX, S, PROF><<<(int)imin64(grid, p.ncol * d->M), 32 * NW, bytes, st>>>(map, p);
+  project_stream_kernel<T, NI, NW, VX, S, PROF><<<(int)imin64((int64_t)grid * DPM_CTAS, p.ncol * d->M), 32 * NW, bytes,
+                                                    st>>>(map, p);
   return DPM_OK;
 }
 
