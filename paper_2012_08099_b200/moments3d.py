@@ -70,8 +70,10 @@ def _count(counters: OpCounters | None, order: int, dims) -> None:
     from .engine import num_images
     l, m, n = dims
     p = num_images(order)
-    counters.additions += p * l * m * n                     # projection pass
-    px = l * m + m * n + n * l + max(0, p - 3) * (l + 2 * n) * m
+    counters.additions += p * l * m * n                     # projection pass: P - 1 images + the profile
+    widths = [l + n - 1, l + n - 1, l + 2 * n - 2, l + 2 * n - 2][: p - 3]
+    t = {3: 1, 4: 2, 5: 2, 6: 3}[order]
+    px = l * m + m * n + sum(widths) * m + (l + t * (n - 1))  # image pixels + profile cells
     counters.multiplications += (order + 1) * px              # row-power products
     counters.additions += (order + 1) * px
 
