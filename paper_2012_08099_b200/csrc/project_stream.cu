@@ -15,14 +15,24 @@
 //   CTA      = NW warps, warp w owns planes Z0+8w..+7, lane l owns x = X0+VX*l..+VX-1:
 //              each lane reduces a VX (x) x 8 (z) patch per row-step (VX = 8, or
 //              4 for narrow volumes such as the 128^3 batch).  NW = 12 (3 warps
-//              per scheduler, <= 168 registers; 16 for 4-wide lanes at order 3);
-//              at order 6 the (x +- 2z) images are folded in a second pass over
-//              the same stage to stay within that budget.  The TMA producer is
-//              lane 0 of warp NW/2 (the row flush lands on warps 0-3).
-//   ZX (x,z)  sum over y: 8*VX registers per lane, persistent across the
+//              per scheduler, <= 168 registers; 16 for 4-wide lanes at order 3).
+//              The TMA producer is lane 0 of warp NW/2 (the row flush lands on
+//              warps 0-3).
+//   Two modes (template PROF):
+//   PROF = 0 (dpm_project: the reference's images)
+//     ZX (x,z) sum over y: 8*VX registers per lane, persistent across the
 //             row-steps of a column (adds on the FMA pipe), flushed at the end
 //             of the CTA's run through the column: an 8x8 shfl.xor transpose
 //             per 8-lane group makes every red.global cover 32-byte runs of z.
+//             At order 6 the (x +- 2z) images are folded in a second pass over
+//             the same stage to stay within the register budget.
+//   PROF = 1 (the moments pipeline)
+//     no ZX; the profile P[x + t z] = sum_y V (t = -1, 2, -2, 3 at 4..7 images)
+//             is a VX + 7|t| register window folded with IMAD-by-1 (FMA pipe),
+//             summed over the rows of a column run, then added to a CTA shared
+//             row (conflict-free transposed layout) and to the uint64 global
+//             profile with one coalesced pass of atomics per column and y-band.
+//             Order 6 runs in one pass.
 //   XY and the oblique images (x + t z, y), t = 1, -1, 2, -2: plane pairs are
 //             folded into VX / VX+7 / VX+14-cell register windows with 3-input
 //             adds, and every lane adds its WHOLE window to the CTA row with
