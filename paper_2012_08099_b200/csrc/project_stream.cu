@@ -108,13 +108,19 @@ template <int VX> struct Unpack<uint16_t, VX> {
     }
   }
 };
+// signed 16-bit plus offset: lo half sign-extended by one PRMT (sign-replicate
+// selector), hi half by an arithmetic shift, then the offset.  The caller
+// passes off = 0 for out-of-bounds planes / lanes, whose TMA zero fill must
+// stay 0 -- one select per plane instead of one per voxel.
 template <int VX> struct Unpack<int16_t, VX> {
   template <typename V> __device__ __forceinline__ static void run(const V& d, uint32_t* v, int32_t off, uint32_t) {
     const uint32_t* w = reinterpret_cast<const uint32_t*>(&d);
     #pragma unroll
     for (int i = 0; i < VX / 2; ++i) {
-      v[2 * i] = (uint32_t)((int32_t)(int16_t)(w[i] & 0xFFFFu) + off);
-      v[2 * i + 1] = (uint32_t)((int32_t)(int16_t)(w[i] >> 16) + off);
+      uint32_t lo;   // prmt with sign-replicate selector nibbles (__byte_perm ignores the sign bit)
+      asm("prmt.b32 %0, %1, 0, 0x9910;" : "=r"(lo) : "r"(w[i]));
+      v[2 * i] = lo + (uint32_t)off;
+      v[2 * i + 1] = (uint32_t)((int32_t)w[i] >> 16) + (uint32_t)off;
     }
   }
 };
@@ -566,13 +572,9 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
         for (int t = 2 * tp + 2; t < 2 * tp + 4; ++t) dv[t] = *reinterpret_cast<const V*>(tile + t * SX);
       }
       uint32_t a[VX], bb[VX];
-      Unpack<T, VX>::run(dv[t0], a, p.offset, p.one << 16);
-      Unpack<T, VX>::run(dv[t1], bb, p.offset, p.one << 16);
-      if (((T)-1) < (T)0) {  // signed input: zero-filled (out-of-bounds) voxels must stay 0 after the offset
-        const bool ok0 = g.xok && t0 < g.zc, ok1 = g.xok && t1 < g.zc;
-        #pragma unroll
-        for (int k = 0; k < VX; ++k) { a[k] = ok0 ? a[k] : 0u; bb[k] = ok1 ? bb[k] : 0u; }
-      }
+      // signed input: out-of-bounds (zero-filled) voxels get no offset
+      Unpack<T, VX>::run(dv[t0], a, g.xok && t0 < g.zc ? p.offset : 0, p.one << 16);
+      Unpack<T, VX>::run(dv[t1], bb, g.xok && t1 < g.zc ? p.offset : 0, p.one << 16);
       #pragma unroll
       for (int k = 0; k < VX; ++k) {
         if constexpr (!PROF) {
@@ -639,13 +641,10 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
         for (int tp = 0; tp < 4; ++tp) {
           const int t0 = 2 * tp, t1 = t0 + 1;
           uint32_t a[VX], bb[VX];
-          Unpack<T, VX>::run(*reinterpret_cast<const V*>(tile + t0 * SX), a, p.offset, p.one << 16);
-          Unpack<T, VX>::run(*reinterpret_cast<const V*>(tile + t1 * SX), bb, p.offset, p.one << 16);
-          if (((T)-1) < (T)0) {
-            const bool ok0 = g.xok && t0 < g.zc, ok1 = g.xok && t1 < g.zc;
-            #pragma unroll
-            for (int k = 0; k < VX; ++k) { a[k] = ok0 ? a[k] : 0u; bb[k] = ok1 ? bb[k] : 0u; }
-          }
+          Unpack<T, VX>::run(*reinterpret_cast<const V*>(tile + t0 * SX), a, g.xok && t0 < g.zc ? p.offset : 0,
+                             p.one << 16);
+          Unpack<T, VX>::run(*reinterpret_cast<const V*>(tile + t1 * SX), bb, g.xok && t1 < g.zc ? p.offset : 0,
+                             p.one << 16);
           fold<2, N2, VX>(wp, a, bb, 2 * t0, 2 * t0 + 2, p.one);
           fold<3, N2, VX>(wm, a, bb, 14 - 2 * t0, 12 - 2 * t0, p.one);
         }

@@ -32,14 +32,20 @@ def main():
              ("1024^3 u16 K4", (1024, 1024, 1024), torch.uint16, 4),
              ("1024^3 u8 K3", (1024, 1024, 1024), torch.uint8, 3),
              ("cfg5 2048^3 u16 K6", (2048, 2048, 2048), torch.uint16, 6),
-             ("cfg4 1024x128^3 u8 K3", (1024, 128, 128, 128), torch.uint8, 3)]
+             ("cfg4 1024x128^3 u8 K3", (1024, 128, 128, 128), torch.uint8, 3),
+             ("cfg3 512^3 i16+1024 K4", (512, 512, 512), torch.int16, 4)]
     for name, shape, dt, K in cases:
         if only and only not in name:
             continue
         n = 1
         for d in shape:
             n *= d
-        if len(shape) == 4:
+        off = 0
+        if dt == torch.int16:
+            from paper_2012_08099_b200 import configs
+            v = torch.from_numpy(configs.cfg3(0)).cuda()
+            off = 1024
+        elif len(shape) == 4:
             v = (torch.rand(shape, device="cuda") < 0.3).to(torch.uint8)
         elif dt == torch.uint16:
             v = engine.synth_noise(shape[2], shape[1], 0, shape[0], 5)
@@ -47,7 +53,7 @@ def main():
             v = torch.randint(0, 256, shape, dtype=torch.uint8, device="cuda")
         nbytes = v.numel() * v.element_size()
         if profile_only:
-            tq = timeit(lambda: engine.project_profile(v, K))
+            tq = timeit(lambda: engine.project_profile(v, K, off))
             print(f"{name}: project_profile {tq:.3f} ms ({nbytes / tq / 1e6:.0f} GB/s)", flush=True)
             continue
         tp = timeit(lambda: engine.project(v, engine.num_images(K)))
