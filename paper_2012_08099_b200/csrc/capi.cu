@@ -15,9 +15,8 @@ int launch_project_stream(const dpm_volume_desc* d, const void* vox, const Image
                           cudaStream_t st, bool* handled);
 int profile_shift(int n_img);
 size_t project_stream_workspace(const dpm_volume_desc* d, int n_img);
-int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_t* acc, cudaStream_t st);
-int launch_profile_moments(const unsigned long long* prof, int64_t WQ, int64_t B, int64_t ai, int order, int n_img,
-                           int slot, uint64_t* acc, cudaStream_t st);
+int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_t* acc, cudaStream_t st,
+                     const M2Extra* ex = nullptr);
 int launch_derive3d(const uint64_t* acc, int64_t B, int n_img, int order, int kind, int64_t* out_i128,
                     double* out_f64, int32_t* status, cudaStream_t st);
 int launch_synth_noise(uint16_t* out, int64_t L, int64_t M, int64_t z0, int64_t nz, uint64_t seed, cudaStream_t st);
@@ -176,18 +175,27 @@ static int project_profile_launch(const dpm_volume_desc* desc, const void* d_vox
   return launch_project_generic(desc, d_voxels, s, prof, st);
 }
 
-// image + profile moments into an already zeroed DPM_ACC_PROFILE accumulator
+// image + profile moments (one launch) into an already zeroed DPM_ACC_PROFILE
+// accumulator; with `fused` (counters zeroed, outputs) the same launch ends
+// with the epilogue
+struct FusedOut { unsigned int* cnt; int64_t* i128; double* f64; int32_t* status; };
 static int moments2d_profile_launch(const dpm_volume_desc* desc, int order, const uint32_t* const* d_images,
-                                    const uint64_t* d_profile, uint64_t* d_acc, cudaStream_t st) {
+                                    const uint64_t* d_profile, uint64_t* d_acc, cudaStream_t st,
+                                    const FusedOut* fused = nullptr) {
   const int n_img = num_images(order);
   ImageSet s = make_set(desc, n_img, const_cast<uint32_t* const*>(d_images), true);
   const int jb = jbits_for(desc, n_img);
   if (jb > 21) return DPM_EOVERFLOW;
-  int rc = launch_moments2d(s, desc->B, order, jb, d_acc, st);
-  if (rc) return rc;
   const ProfGeom pg = profile_geom(desc, order);
-  return launch_profile_moments(reinterpret_cast<const unsigned long long*>(d_profile), pg.WQ, desc->B, pg.ai, order,
-                                n_img, DPM_IMG_ZX, d_acc, st);
+  M2Extra ex;
+  ex.prof = reinterpret_cast<const unsigned long long*>(d_profile);
+  ex.WQ = pg.WQ;
+  ex.ai = pg.ai;
+  ex.cnt = fused ? fused->cnt : nullptr;
+  ex.out_i128 = fused ? fused->i128 : nullptr;
+  ex.out_f64 = fused ? fused->f64 : nullptr;
+  ex.status = fused ? fused->status : nullptr;
+  return launch_moments2d(s, desc->B, order, jb, d_acc, st, &ex);
 }
 
 int dpm_project_profile(const dpm_volume_desc* desc, const void* d_voxels, int order, uint32_t* const* d_images,
@@ -231,8 +239,11 @@ size_t dpm_partial_workspace_bytes(const dpm_volume_desc* desc, int order) {
 
 // acc_adjacent: d_acc is the acc_bytes_of() bytes right before d_ws (dpm_moments'
 // own workspace carve), so one memset zeroes accumulator, images and profile
+// fused (dpm_moments): the volume counters follow the partial scratch in the
+// same workspace, and the moments launch ends with the epilogue
 static int moments_partial_impl(const dpm_volume_desc* desc, const void* d_voxels, int order, void* d_ws,
-                                size_t ws_bytes, uint64_t* d_acc, void* stream, bool acc_adjacent) {
+                                size_t ws_bytes, uint64_t* d_acc, void* stream, bool acc_adjacent,
+                                const FusedOut* fused = nullptr) {
   int rc = check_desc(desc);
   if (rc) return rc;
   if (check_order(order) || !d_voxels || !d_acc) return DPM_EINVAL;
@@ -248,7 +259,8 @@ static int moments_partial_impl(const dpm_volume_desc* desc, const void* d_voxel
   // one zeroing of the contiguous images + profile scratch, one of the accumulator
   // (or none when the caller's accumulator directly precedes it: dpm_moments)
   char* z0 = acc_adjacent ? reinterpret_cast<char*>(d_acc) : base;
-  const size_t zb = dpm_partial_workspace_bytes(desc, order) + (acc_adjacent ? acc_bytes_of(desc, order) : 0);
+  const size_t zb = dpm_partial_workspace_bytes(desc, order) + (acc_adjacent ? acc_bytes_of(desc, order) : 0) +
+                    (fused ? align256((size_t)desc->B * sizeof(unsigned int)) : 0);
   if (cudaMemsetAsync(z0, 0, zb, st) != cudaSuccess) return DPM_ECUDA;
   if (!acc_adjacent &&
       cudaMemsetAsync(d_acc, 0, (size_t)(desc->B * n_img * n2d(order) * 4) * sizeof(uint64_t), st) != cudaSuccess)
@@ -256,7 +268,7 @@ static int moments_partial_impl(const dpm_volume_desc* desc, const void* d_voxel
   reset_launches();
   rc = project_profile_launch(desc, d_voxels, order, imgs, prof, st);
   if (rc) return rc;
-  return moments2d_profile_launch(desc, order, imgs, prof, d_acc, st);
+  return moments2d_profile_launch(desc, order, imgs, prof, d_acc, st, fused);
 }
 
 int dpm_moments_partial(const dpm_volume_desc* desc, const void* d_voxels, int order, void* d_ws, size_t ws_bytes,
@@ -308,7 +320,7 @@ size_t dpm_workspace_bytes(const dpm_volume_desc* desc, int order) {
   if (check_desc(desc) || check_order(order)) return 0;
   const int n_img = num_images(order);
   return align256((size_t)(desc->B * n_img * n2d(order) * 4) * sizeof(uint64_t)) +
-         dpm_partial_workspace_bytes(desc, order);
+         dpm_partial_workspace_bytes(desc, order) + align256((size_t)desc->B * sizeof(unsigned int));
 }
 
 int dpm_check_envelope(int64_t L, int64_t M, int64_t N_global, int64_t vmax, int order) {
@@ -338,15 +350,15 @@ int dpm_moments(const dpm_volume_desc* desc, const void* d_voxels, int order, vo
   if (ws_bytes < dpm_workspace_bytes(desc, order) || !d_ws) return DPM_EWORKSPACE;
   uint64_t* acc = static_cast<uint64_t*>(d_ws);
   const size_t acc_bytes = acc_bytes_of(desc, order);
-  int launches = 0;
-  rc = moments_partial_impl(desc, d_voxels, order, static_cast<char*>(d_ws) + acc_bytes, ws_bytes - acc_bytes, acc,
-                            stream, true);
-  launches += dpm_last_launch_count();
-  if (rc) return rc;
-  rc = dpm_derive3d(desc, acc, order, DPM_ACC_PROFILE, d_m3d_i128, d_m3d_f64, d_status, stream);
-  launches += dpm_last_launch_count();
-  g_launches = launches;
-  return rc;
+  char* pws = static_cast<char*>(d_ws) + acc_bytes;
+  const size_t pbytes = dpm_partial_workspace_bytes(desc, order);
+  FusedOut f;
+  f.cnt = reinterpret_cast<unsigned int*>(pws + pbytes);
+  f.i128 = d_m3d_i128;
+  f.f64 = d_m3d_f64;
+  f.status = d_status;
+  // memset, projection pass, one moments launch that ends with the epilogue
+  return moments_partial_impl(desc, d_voxels, order, pws, ws_bytes - acc_bytes, acc, stream, true, &f);
 }
 
 int dpm_acc_add(uint64_t* d_acc_out, const uint64_t* d_acc_in, int64_t count, void* stream);

@@ -58,6 +58,18 @@ template <> struct VoxelTraits<uint8_t>  { static __device__ __forceinline__ uin
 template <> struct VoxelTraits<uint16_t> { static __device__ __forceinline__ uint32_t get(uint16_t v, int32_t) { return v; } };
 template <> struct VoxelTraits<int16_t>  { static __device__ __forceinline__ uint32_t get(int16_t v, int32_t off) { return (uint32_t)((int32_t)v + off); } };
 
+// Optional parts of the moments kernel launch (launch_moments2d): the
+// profile's 1D moments in the same grid, and the fused epilogue (the last
+// block of each volume runs derive_volume; cnt[B] zeroed by the caller).
+struct M2Extra {
+  const unsigned long long* prof;
+  int64_t WQ, ai;
+  unsigned int* cnt;
+  int64_t* out_i128;
+  double* out_f64;
+  int32_t* status;
+};
+
 // thread-local count of kernels the last C-ABI call enqueued
 void note_launches(int n);
 void reset_launches();

@@ -17,7 +17,7 @@
 // The host checks the exactness envelope first (dpm_check_envelope), so every
 // partial sum is below 2^126 and arithmetic mod 2^128 is exact.
 #include <mutex>
-#include "dpm_common.cuh"
+#include "derive_dev.cuh"
 
 namespace dpm {
 
@@ -36,7 +36,53 @@ struct M2Params {
   int64_t blocks_img[DPM_MAX_IMAGES + 1];  // prefix sums of blocks per image (per volume)
   int64_t cblocks[DPM_MAX_IMAGES];         // column blocks per image
   uint64_t* acc;                           // [B][n_img][n2][4]
+  // moments pipeline: the profile's 1D moments in the same launch (pblocks
+  // extra blocks per volume, into the q = 0 entries of slot DPM_IMG_ZX)
+  const unsigned long long* prof;          // [B][WQ] or null
+  int64_t WQ, prof_ai, pblocks;
+  // fused epilogue: the last block of each volume (counter cnt[b], zeroed by
+  // the caller) runs derive_volume for it; null out_i128 = separate derive3d
+  unsigned int* cnt;
+  int64_t* out_i128;
+  double* out_f64;
+  int32_t* status;
 };
+
+// one block's share of the profile's 1D moments (cells chunk, chunk + pblocks, ...)
+template <int K>
+__device__ __forceinline__ void profile_block(const M2Params& p, int64_t b, int64_t chunk, int tid) {
+  constexpr int N2 = (K + 1) * (K + 2) / 2;
+  uint64_t l[K + 1][4];
+  #pragma unroll
+  for (int a = 0; a <= K; ++a) { l[a][0] = l[a][1] = l[a][2] = l[a][3] = 0; }
+  for (int64_t i = chunk * M2_THREADS + tid; i < p.WQ; i += p.pblocks * M2_THREADS) {
+    const unsigned long long v = p.prof[b * p.WQ + i];
+    if (v == 0) continue;
+    const __int128 x = (__int128)(i + p.prof_ai);
+    __int128 pw = 1;
+    #pragma unroll
+    for (int a = 0; a <= K; ++a) {
+      const unsigned __int128 t = (unsigned __int128)v * (unsigned __int128)pw;
+      l[a][0] += (uint32_t)t;
+      l[a][1] += (uint32_t)(t >> 32);
+      l[a][2] += (uint32_t)(t >> 64);
+      l[a][3] += (uint32_t)(t >> 96);
+      pw *= x;
+    }
+  }
+  uint64_t* out = p.acc + ((b * p.s.n_img + DPM_IMG_ZX) * N2) * 4;
+  #pragma unroll
+  for (int a = 0; a <= K; ++a) {
+    #pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint64_t v = l[a][q];
+      #pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if ((tid & 31) == 0 && v) atomicAdd(reinterpret_cast<unsigned long long*>(out + idx2(K, a, 0) * 4 + q),
+                                          (unsigned long long)v);
+    }
+  }
+}
 
 template <int K, int JB>
 __global__ void __launch_bounds__(M2_THREADS) moments2d_kernel(M2Params p) {
@@ -49,9 +95,14 @@ __global__ void __launch_bounds__(M2_THREADS) moments2d_kernel(M2Params p) {
   uint32_t (*table)[NTP] = reinterpret_cast<uint32_t (*)[NTP]>(m2_smem);
   uint32_t (*red)[M2_THREADS + 1] = reinterpret_cast<uint32_t (*)[M2_THREADS + 1]>(m2_smem);
 
-  const int64_t per_vol = p.blocks_img[p.s.n_img];
+  const int64_t per_img = p.blocks_img[p.s.n_img];
+  const int64_t per_vol = per_img + p.pblocks;
   const int64_t b = blockIdx.x / per_vol;
   int64_t r = blockIdx.x - b * per_vol;
+  const int tid = threadIdx.x;
+  if (r >= per_img) {
+    profile_block<K>(p, b, r - per_img, tid);
+  } else {
   int k = 0;
   while (r >= p.blocks_img[k + 1]) ++k;
   r -= p.blocks_img[k];
@@ -59,7 +110,6 @@ __global__ void __launch_bounds__(M2_THREADS) moments2d_kernel(M2Params p) {
   const int64_t W = p.s.W[k], H = p.s.H[k], ai = p.s.ai[k], aj = p.s.aj[k];
   const int64_t j0 = rb * p.rc;
   const int rows = (int)imin64(p.rc, H - j0);
-  const int tid = threadIdx.x;
 
   // row-power limb table: (j + aj)^q as 24-bit limbs
   for (int rr = tid; rr < rows; rr += M2_THREADS) {
@@ -151,6 +201,22 @@ __global__ void __launch_bounds__(M2_THREADS) moments2d_kernel(M2Params p) {
     }
     __syncthreads();
   }
+  }   // image block
+  if (p.out_i128) {   // fused epilogue: the volume's last block derives its 3D moments
+    __shared__ int last;
+    __shared__ int32_t sst;
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      last = atomicAdd(p.cnt + b, 1u) == (unsigned)(per_vol - 1);
+    }
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      derive_volume<K>(p.acc + b * p.s.n_img * N2 * 4, b, p.s.n_img, DPM_ACC_PROFILE, p.out_i128, p.out_f64,
+                       p.status, reinterpret_cast<uint64_t*>(m2_smem), &sst, true);
+    }
+  }
 }
 
 template <int K, int JB>
@@ -174,9 +240,18 @@ static void launch_k(int jb, dim3 grid, cudaStream_t st, const M2Params& p) {
   else launch_kj<K, 21>(grid, st, p);
 }
 
-int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_t* acc, cudaStream_t st) {
+int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_t* acc, cudaStream_t st,
+                     const M2Extra* ex) {
   M2Params p;
   p.s = s; p.B = B; p.acc = acc;
+  p.prof = ex ? ex->prof : nullptr;
+  p.WQ = ex ? ex->WQ : 0;
+  p.prof_ai = ex ? ex->ai : 0;
+  p.pblocks = p.prof ? imin64((p.WQ + M2_THREADS - 1) / M2_THREADS, 16) : 0;
+  p.cnt = ex ? ex->cnt : nullptr;
+  p.out_i128 = ex ? ex->out_i128 : nullptr;
+  p.out_f64 = ex ? ex->out_f64 : nullptr;
+  p.status = ex ? ex->status : nullptr;
   // rows per chunk: the largest of 256/128/64 that still gives >= 8 CTAs per SM
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -194,7 +269,7 @@ int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_
     p.blocks_img[k + 1] = p.blocks_img[k] + p.cblocks[k] * rblocks;
   }
   for (int k = s.n_img + 1; k <= DPM_MAX_IMAGES; ++k) p.blocks_img[k] = p.blocks_img[s.n_img];
-  const int64_t nblocks = p.blocks_img[s.n_img] * B;
+  const int64_t nblocks = (p.blocks_img[s.n_img] + p.pblocks) * B;
   if (nblocks == 0) return DPM_OK;
   if (nblocks > 0x7fffffffLL) return DPM_EINVAL;
   dim3 grid((unsigned)nblocks);
@@ -203,67 +278,6 @@ int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_
     case 4: launch_k<4>(jbits, grid, st, p); break;
     case 5: launch_k<5>(jbits, grid, st, p); break;
     default: launch_k<6>(jbits, grid, st, p); break;
-  }
-  note_launches(1);
-  DPM_CUDA_CHECK_LAUNCH();
-  return DPM_OK;
-}
-
-// 1D exact moments of the y-summed profile (moments pipeline, DPM_ACC_PROFILE):
-//   M_a = sum_i P[i] (i + ai)^a,  a = 0..K,
-// into the q = 0 entries of accumulator slot `slot` ([B][n_img][n2d][4] limb
-// sums, zeroed by the caller).  Each term is formed mod 2^128 and split into
-// four 32-bit limbs summed in uint64, as in moments2d_kernel.
-constexpr int PM_THREADS = 256;
-
-template <int K>
-__global__ void __launch_bounds__(PM_THREADS) profile_moments_kernel(const unsigned long long* prof, int64_t WQ,
-                                                                    int64_t B, int64_t ai, int n_img, int slot,
-                                                                    uint64_t* acc) {
-  constexpr int N2 = (K + 1) * (K + 2) / 2;
-  for (int64_t b = blockIdx.y; b < B; b += gridDim.y) {
-  uint64_t l[K + 1][4];
-  #pragma unroll
-  for (int a = 0; a <= K; ++a) { l[a][0] = l[a][1] = l[a][2] = l[a][3] = 0; }
-  for (int64_t i = (int64_t)blockIdx.x * PM_THREADS + threadIdx.x; i < WQ; i += (int64_t)gridDim.x * PM_THREADS) {
-    const unsigned long long v = prof[b * WQ + i];
-    if (v == 0) continue;
-    const __int128 x = (__int128)(i + ai);
-    __int128 pw = 1;
-    #pragma unroll
-    for (int a = 0; a <= K; ++a) {
-      const unsigned __int128 t = (unsigned __int128)v * (unsigned __int128)pw;
-      l[a][0] += (uint32_t)t;
-      l[a][1] += (uint32_t)(t >> 32);
-      l[a][2] += (uint32_t)(t >> 64);
-      l[a][3] += (uint32_t)(t >> 96);
-      pw *= x;
-    }
-  }
-  uint64_t* out = acc + ((b * n_img + slot) * N2) * 4;
-  #pragma unroll
-  for (int a = 0; a <= K; ++a) {
-    #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      uint64_t v = l[a][k];
-      #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if ((threadIdx.x & 31) == 0 && v) atomicAdd(reinterpret_cast<unsigned long long*>(out + idx2(K, a, 0) * 4 + k),
-                                                  (unsigned long long)v);
-    }
-  }
-  }
-}
-
-int launch_profile_moments(const unsigned long long* prof, int64_t WQ, int64_t B, int64_t ai, int order, int n_img,
-                           int slot, uint64_t* acc, cudaStream_t st) {
-  const unsigned gx = (unsigned)imin64((WQ + PM_THREADS - 1) / PM_THREADS, 64);
-  const dim3 grid(gx, (unsigned)imin64(B, 65535));
-  switch (order) {
-    case 3: profile_moments_kernel<3><<<grid, PM_THREADS, 0, st>>>(prof, WQ, B, ai, n_img, slot, acc); break;
-    case 4: profile_moments_kernel<4><<<grid, PM_THREADS, 0, st>>>(prof, WQ, B, ai, n_img, slot, acc); break;
-    case 5: profile_moments_kernel<5><<<grid, PM_THREADS, 0, st>>>(prof, WQ, B, ai, n_img, slot, acc); break;
-    default: profile_moments_kernel<6><<<grid, PM_THREADS, 0, st>>>(prof, WQ, B, ai, n_img, slot, acc); break;
   }
   note_launches(1);
   DPM_CUDA_CHECK_LAUNCH();

@@ -114,4 +114,4 @@ def test_graphed_slab_stages(cuda, order):
         res = st.replay_derive()
         torch.cuda.synchronize()
         assert torch.equal(res.i128, engine.derive(want_acc, order).i128)
-    assert st.launches == 4   # projection, image moments, profile moments, epilogue
+    assert st.launches == 3   # projection, image + profile moments, epilogue

@@ -111,4 +111,4 @@ def test_profile_graphed_stages_launches():
     rng = np.random.default_rng(2)
     slab = torch.from_numpy(rng.integers(0, 65535, size=(24, 24, 264)).astype(np.uint16)).cuda()
     st = engine.GraphedSlabStages(slab, 6, z0=16)
-    assert st.launches == 4      # projection, image moments, profile moments, epilogue
+    assert st.launches == 3      # projection, image + profile moments (one launch), epilogue
