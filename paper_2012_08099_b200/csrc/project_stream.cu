@@ -262,9 +262,9 @@ __host__ __device__ constexpr int stride_for(int need, int VX) {
   // smallest S >= need with S = 32/VX (mod 32)
   return ((need - (32 / VX) + 31) / 32) * 32 + (32 / VX);
 }
-template <int NI, int NW, int VX> struct Geo {
+template <int NI, int NW, int VX, int ZP = 8> struct Geo {
   static constexpr int SX = 32 * VX;                   // x-tile
-  static constexpr int SZ = 8 * NW;                    // z-tile
+  static constexpr int SZ = ZP * NW;                   // z-tile (ZP planes per warp)
   static constexpr int W1 = SX + SZ - 1;               // DIAG/ANTI row footprint
   static constexpr int W2 = SX + 2 * SZ - 2;           // X2P/X2M row footprint
   static constexpr int SXY = stride_for(32 + 1, VX);
@@ -288,13 +288,14 @@ struct ColGeom {
   int32_t b;
   int zc;
   bool xok;
-  __device__ __forceinline__ void set(const StreamParams& p, int32_t col, int SX, int SZ, int VX, int w, int lane) {
+  __device__ __forceinline__ void set(const StreamParams& p, int32_t col, int SX, int SZ, int VX, int ZP, int w,
+                                      int lane) {
     const int32_t per = (int32_t)(p.ntz * p.ntx);
     b = col / per;
     const int32_t r = col - b * per;
     Z0 = (int64_t)(r / (int32_t)p.ntx) * SZ;
     X0 = (int64_t)(r % (int32_t)p.ntx) * SX;
-    zc = (int)imax64(0, imin64(8, p.N - (Z0 + 8 * w)));
+    zc = (int)imax64(0, imin64(ZP, p.N - (Z0 + ZP * w)));
     xok = X0 + VX * lane < p.L;
   }
 };
@@ -348,16 +349,16 @@ struct RegionCol {
   }
 };
 
-template <typename T, int NI, int NW, int VX, int STAGES, bool PROF>
-#ifndef DPM_CTAS
-#define DPM_CTAS 1   // resident CTAs per SM (the 12 / 16 warps of an SM split over them)
-#endif
-__global__ void __launch_bounds__(32 * NW, DPM_CTAS)
+// ZP: planes per warp (8, or 16 for the 4-wide-lane batch variant, profile
+// mode only); CTAS: resident CTAs per SM
+template <typename T, int NI, int NW, int VX, int STAGES, bool PROF, int ZP, int CTAS>
+__global__ void __launch_bounds__(32 * NW, CTAS)
 project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
-  using G = Geo<NI, NW, VX>;
+  static_assert(ZP == 8 || (ZP == 16 && PROF && NI <= 5), "16-plane warps: profile mode, orders <= 4");
+  using G = Geo<NI, NW, VX, ZP>;
   using V = typename Vec<T, VX>::type;
   constexpr int SX = G::SX, SZ = G::SZ, THREADS = G::THREADS;
-  constexpr int N1 = VX + 7, N2 = VX + 14;             // oblique window widths
+  constexpr int N1 = VX + ZP - 1, N2 = VX + 2 * (ZP - 1);   // oblique window widths
 #ifndef DPM_PROF_TWO_PASS
 #define DPM_PROF_TWO_PASS 0
 #endif
@@ -365,7 +366,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
   // for them in the first); the profile mode frees those registers
   constexpr bool TWO_PASS = NI >= 6 && VX == 8 && NW > 8 && (!PROF || DPM_PROF_TWO_PASS);
   constexpr int TQ = ProfT<NI>::value, AQ = TQ < 0 ? -TQ : TQ;
-  constexpr int NQ = PROF ? VX + 7 * AQ : 1;           // profile window width
+  constexpr int NQ = PROF ? VX + (ZP - 1) * AQ : 1;    // profile window width
   constexpr uint32_t STAGE_BYTES = SX * SZ * sizeof(T);
   constexpr int YZT = G::YZT;   // words of one YZ tile (0: YZ goes straight to global)
   // TMA producer: lane 0 of a middle warp.  The row flushes start at thread 0,
@@ -497,7 +498,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     if constexpr (PROF) {
       if (col < 0) return;
       const uint32_t pa = ptx::smem_addr(prow) + 4u * lane;
-      const int lb = TQ > 0 ? 8 * w * TQ : 8 * (NW - 1 - w) * AQ;   // warp's first row cell - VX*lane
+      const int lb = TQ > 0 ? ZP * w * TQ : ZP * (NW - 1 - w) * AQ;   // warp's first row cell - VX*lane
       #pragma unroll
       for (int c = 0; c < NQ; ++c) {
         const int i = lb + c;   // + VX * lane
@@ -525,7 +526,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     if (cur.c != col) {
       flush_zx();
       col = cur.c;
-      g.set(p, col, SX, SZ, VX, w, lane);
+      g.set(p, col, SX, SZ, VX, ZP, w, lane);
       if constexpr (!PROF) {
         #pragma unroll
         for (int t = 0; t < 8; ++t) {
@@ -533,8 +534,8 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
           for (int k = 0; k < VX; ++k) zx[t][k] = 0;
         }
       }
-      zx_col = p.s.img[DPM_IMG_ZX] + (int64_t)g.b * p.L * p.N + (g.X0 + VX * lane) * p.N + g.Z0 + 8 * w;
-      yz_col = p.s.img[DPM_IMG_YZ] + (int64_t)g.b * p.M * p.N + (g.Z0 + 8 * w + (lane & 7)) * p.M;
+      zx_col = p.s.img[DPM_IMG_ZX] + (int64_t)g.b * p.L * p.N + (g.X0 + VX * lane) * p.N + g.Z0 + ZP * w;
+      yz_col = p.s.img[DPM_IMG_YZ] + (int64_t)g.b * p.M * p.N + (g.Z0 + ZP * w + (lane & (ZP - 1))) * p.M;
       rslot ^= 1;
       if (tid == 0) {
         RegionCol* rc = rcs + 5 * rslot;
@@ -550,7 +551,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     for (int32_t y = y_first; y < y_end; ++y) {
     if (g.zc > 0) {   // warp-uniform: warps past the volume's last plane only join the barrier
     ptx::mbar_wait_addr(full_addr + 8u * cst, cphase);
-    const T* tile = reinterpret_cast<const T*>(stages + cst * STAGE_BYTES) + (8 * w) * SX + VX * lane;
+    const T* tile = reinterpret_cast<const T*>(stages + cst * STAGE_BYTES) + (ZP * w) * SX + VX * lane;
 
     uint32_t cs[VX];
     uint32_t yzmine = 0;   // lane t < 8: this warp's plane t sum (YZ), reduced as each plane pair is folded
@@ -561,13 +562,13 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     for (int i = 0; i < N1; ++i) { wd[i] = 0; wa[i] = 0; }
     #pragma unroll
     for (int i = 0; i < N2; ++i) { wp[i] = 0; wm[i] = 0; }
-    V dv[8];
+    V dv[ZP];
     #pragma unroll
     for (int t = 0; t < 4; ++t) dv[t] = *reinterpret_cast<const V*>(tile + t * SX);
     #pragma unroll
-    for (int tp = 0; tp < 4; ++tp) {
+    for (int tp = 0; tp < ZP / 2; ++tp) {
       const int t0 = 2 * tp, t1 = t0 + 1;
-      if (tp >= 1 && tp <= 2) {   // two plane pairs in flight (16 fewer live registers than all 8 up front)
+      if (tp >= 1 && 2 * tp + 3 < ZP) {   // two plane pairs in flight (16 fewer live registers than all 8 up front)
         #pragma unroll
         for (int t = 2 * tp + 2; t < 2 * tp + 4; ++t) dv[t] = *reinterpret_cast<const V*>(tile + t * SX);
       }
@@ -589,10 +590,10 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
         constexpr int ALU_PAIRS = NI >= 7 ? 0 : 8;
         if (((ALU_PAIRS >> tp) & 1) != 0) {
           if (TQ > 0) fold_pair<NQ, VX>(wq, a, bb, TQ * t0, TQ * t1);
-          else fold_pair<NQ, VX>(wq, a, bb, AQ * (7 - t0), AQ * (7 - t1));
+          else fold_pair<NQ, VX>(wq, a, bb, AQ * (ZP - 1 - t0), AQ * (ZP - 1 - t1));
         } else {
           if (TQ > 0) fold<4, NQ, VX>(wq, a, bb, TQ * t0, TQ * t1, p.one);
-          else fold<4, NQ, VX>(wq, a, bb, AQ * (7 - t0), AQ * (7 - t1), p.one);
+          else fold<4, NQ, VX>(wq, a, bb, AQ * (ZP - 1 - t0), AQ * (ZP - 1 - t1), p.one);
         }
       }
       {   // YZ: warp-wide redux of the plane sums (one REDUX per plane)
@@ -608,16 +609,16 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
         }
       }
       fold<0, N1, VX>(wd, a, bb, t0, t0 + 1, p.one);
-      if (NI > DPM_IMG_ANTI) fold<1, N1, VX>(wa, a, bb, 7 - t0, 6 - t0, p.one);
+      if (NI > DPM_IMG_ANTI) fold<1, N1, VX>(wa, a, bb, ZP - 1 - t0, ZP - 2 - t0, p.one);
       if (!TWO_PASS && NI > DPM_IMG_X2P) fold<2, N2, VX>(wp, a, bb, 2 * t0, 2 * t0 + 2, p.one);
-      if (!TWO_PASS && NI > DPM_IMG_X2M) fold<3, N2, VX>(wm, a, bb, 14 - 2 * t0, 12 - 2 * t0, p.one);
+      if (!TWO_PASS && NI > DPM_IMG_X2M) fold<3, N2, VX>(wm, a, bb, 2 * (ZP - 1) - 2 * t0, 2 * (ZP - 2) - 2 * t0, p.one);
     }
 
     // ---- YZ: lane t < 8 holds plane t of this warp (reduced in the fold loop)
     if (YZT > 0) {
-      if (lane < 8) yzb[yzpar * SZ * 8 + (8 * w + lane) * 8 + (y & 7)] = yzmine;
+      if (lane < ZP) yzb[yzpar * SZ * 8 + (ZP * w + lane) * 8 + (y & 7)] = yzmine;
     } else {
-      ptx::red_global_add_if(yz_col + y, yzmine, lane < 8 && yzmine != 0 && lane < g.zc);
+      ptx::red_global_add_if(yz_col + y, yzmine, lane < ZP && yzmine != 0 && lane < g.zc);
     }
 
     // ---- add the XY column sums and the oblique windows to the CTA rows
@@ -625,11 +626,11 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
       const uint32_t rp = rows_addr + (uint32_t)(parity * G::WORDS * 4);
       add_owned<G::SXY, VX>(rp + 4 * (G::XY + lane), cs);
       {
-        const uint32_t base = rp + 4 * (G::DG + lane + (8 / VX) * w);
+        const uint32_t base = rp + 4 * (G::DG + lane + (ZP / VX) * w);
         add_window<G::SOB, VX, N1>(base, wd);
       }
       if (NI > DPM_IMG_ANTI) {
-        const uint32_t base = rp + 4 * (G::AN + lane + (8 / VX) * (NW - 1 - w));
+        const uint32_t base = rp + 4 * (G::AN + lane + (ZP / VX) * (NW - 1 - w));
         add_window<G::SOB, VX, N1>(base, wa);
       }
       if (TWO_PASS) {
@@ -650,11 +651,11 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
         }
       }
       if (NI > DPM_IMG_X2P) {
-        const uint32_t base = rp + 4 * (G::XP + lane + (16 / VX) * w);
+        const uint32_t base = rp + 4 * (G::XP + lane + (2 * ZP / VX) * w);
         add_window<G::SOB, VX, N2>(base, wp);
       }
       if (NI > DPM_IMG_X2M) {
-        const uint32_t base = rp + 4 * (G::XM + lane + (16 / VX) * (NW - 1 - w));
+        const uint32_t base = rp + 4 * (G::XM + lane + (2 * ZP / VX) * (NW - 1 - w));
         add_window<G::SOB, VX, N2>(base, wm);
       }
     }
@@ -743,27 +744,38 @@ size_t project_stream_workspace(const dpm_volume_desc*, int) { return 0; }
 // warps per CTA: 12 (3 warps/SMSP, <= 168 registers) unless the 8-wide lanes
 // of orders >= 5 need more registers (then 8 warps, <= 255 registers); the
 // 4-wide lanes of order 3 fit 128 registers, so 16 warps (128-plane z-tiles)
-template <int NI, int VX> struct WarpsFor {
-  static constexpr int value = ((VX == 4 && NI == 4) ? 16 : 12) / DPM_CTAS;
+#ifndef DPM_BATCH_ZP
+#define DPM_BATCH_ZP 16  // planes per warp of the 4-wide-lane order-3 profile variant: 16 = 8 warps x 2 CTAs/SM (v27)
+#endif
+template <int NI, int VX, bool PROF> struct CfgFor {
+  static constexpr bool batch16 = DPM_BATCH_ZP == 16 && VX == 4 && NI == 4 && PROF;
+  static constexpr int ZP = batch16 ? 16 : 8;
+  static constexpr int CTAS = batch16 ? 2 : 1;
+  static constexpr int NW = batch16 ? 8 : (VX == 4 && NI == 4) ? 16 : 12;
+};
+template <int NI, int VX, bool PROF = false> struct WarpsFor {
+  static constexpr int value = CfgFor<NI, VX, PROF>::NW;
 };
 // stages: as many 4-D boxes as fit next to the row buffers
 template <typename T, int NI, int VX, bool PROF> struct StagesFor {
-  static constexpr int NW = WarpsFor<NI, VX>::value;
-  static constexpr int BOX = 32 * VX * 8 * NW * (int)sizeof(T);
-  static constexpr int ROWS = 2 * Geo<NI, NW, VX>::WORDS * 4 + 2 * Geo<NI, NW, VX>::YZT * 4 +
-                              (PROF ? Geo<NI, NW, VX>::PW * 4 : 0);
-  static constexpr int FIT = ((DPM_CTAS == 1 ? 220 : 111) * 1024 - ROWS) / BOX;
+  using C = CfgFor<NI, VX, PROF>;
+  static constexpr int NW = C::NW;
+  using GG = Geo<NI, NW, VX, C::ZP>;
+  static constexpr int BOX = 32 * VX * C::ZP * NW * (int)sizeof(T);
+  static constexpr int ROWS = 2 * GG::WORDS * 4 + 2 * GG::YZT * 4 + (PROF ? GG::PW * 4 : 0);
+  static constexpr int FIT = ((C::CTAS == 1 ? 220 : 111) * 1024 - ROWS) / BOX;
   static constexpr int value = FIT > 12 ? 12 : FIT;
 };
 
 template <typename T, int NI, int VX, bool PROF>
 static int launch_one(const dpm_volume_desc* d, const void* vox, int grid, cudaStream_t st, StreamParams p) {
-  constexpr int NW = WarpsFor<NI, VX>::value;
+  using C = CfgFor<NI, VX, PROF>;
+  constexpr int NW = C::NW, ZP = C::ZP, CTAS = C::CTAS;
   constexpr int S = StagesFor<T, NI, VX, PROF>::value;
-  using G = Geo<NI, NW, VX>;
+  using G = Geo<NI, NW, VX, ZP>;
   constexpr size_t bytes = (size_t)S * G::SX * G::SZ * sizeof(T) + 2 * G::WORDS * 4 + 2 * G::YZT * 4 + S * 8 + 64 + 160 +
                            (PROF ? G::PW * 4 : 0);
-  static_assert(bytes <= (DPM_CTAS == 1 ? 227 : 112) * 1024, "shared memory budget");
+  static_assert(bytes <= (CTAS == 1 ? 227 : 112) * 1024, "shared memory budget");
   const int64_t es = sizeof(T);
   CUtensorMap map;
   const cuuint64_t dims[4] = {(cuuint64_t)d->L, (cuuint64_t)d->M, (cuuint64_t)d->N, (cuuint64_t)d->B};
@@ -785,11 +797,11 @@ static int launch_one(const dpm_volume_desc* d, const void* vox, int grid, cudaS
   p.ncol = p.ntx * p.ntz * d->B;
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(project_stream_kernel<T, NI, NW, VX, S, PROF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)bytes);
+    cudaFuncSetAttribute(project_stream_kernel<T, NI, NW, VX, S, PROF, ZP, CTAS>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   });
-  project_stream_kernel<T, NI, NW, VX, S, PROF><<<(int)imin64((int64_t)grid * DPM_CTAS, p.ncol * d->M), 32 * NW, bytes,
-                                                    st>>>(map, p);
+  project_stream_kernel<T, NI, NW, VX, S, PROF, ZP, CTAS>
+      <<<(int)imin64((int64_t)grid * CTAS, p.ncol * d->M), 32 * NW, bytes, st>>>(map, p);
   return DPM_OK;
 }
 
