@@ -747,18 +747,23 @@ size_t project_stream_workspace(const dpm_volume_desc*, int) { return 0; }
 #ifndef DPM_BATCH_ZP
 #define DPM_BATCH_ZP 16  // planes per warp of the 4-wide-lane order-3 profile variant: 16 = 8 warps x 2 CTAs/SM (v27)
 #endif
-template <int NI, int VX, bool PROF> struct CfgFor {
+// 8-wide uint8 lanes at orders 3-4 likewise (16 planes, 6 warps x 2 CTAs/SM:
+// 1024^3 u8 K3 -3 %); for uint16 the 2-CTA shared-memory budget leaves 1-2
+// stages of 48 KB, which loses (+20 %) -- tools/EXPERIMENTS.md v28
+#ifndef DPM_WIDE_ZP
+#define DPM_WIDE_ZP 16
+#endif
+template <typename T, int NI, int VX, bool PROF> struct CfgFor {
   static constexpr bool batch16 = DPM_BATCH_ZP == 16 && VX == 4 && NI == 4 && PROF;
-  static constexpr int ZP = batch16 ? 16 : 8;
-  static constexpr int CTAS = batch16 ? 2 : 1;
-  static constexpr int NW = batch16 ? 8 : (VX == 4 && NI == 4) ? 16 : 12;
+  static constexpr bool wide16 = DPM_WIDE_ZP == 16 && VX == 8 && NI <= 5 && PROF && sizeof(T) == 1;
+  static constexpr int ZP = (batch16 || wide16) ? 16 : 8;
+  static constexpr int CTAS = (batch16 || wide16) ? 2 : 1;
+  static constexpr int NW = batch16 ? 8 : wide16 ? 6 : (VX == 4 && NI == 4) ? 16 : 12;
 };
-template <int NI, int VX, bool PROF = false> struct WarpsFor {
-  static constexpr int value = CfgFor<NI, VX, PROF>::NW;
-};
+
 // stages: as many 4-D boxes as fit next to the row buffers
 template <typename T, int NI, int VX, bool PROF> struct StagesFor {
-  using C = CfgFor<NI, VX, PROF>;
+  using C = CfgFor<T, NI, VX, PROF>;
   static constexpr int NW = C::NW;
   using GG = Geo<NI, NW, VX, C::ZP>;
   static constexpr int BOX = 32 * VX * C::ZP * NW * (int)sizeof(T);
@@ -769,7 +774,7 @@ template <typename T, int NI, int VX, bool PROF> struct StagesFor {
 
 template <typename T, int NI, int VX, bool PROF>
 static int launch_one(const dpm_volume_desc* d, const void* vox, int grid, cudaStream_t st, StreamParams p) {
-  using C = CfgFor<NI, VX, PROF>;
+  using C = CfgFor<T, NI, VX, PROF>;
   constexpr int NW = C::NW, ZP = C::ZP, CTAS = C::CTAS;
   constexpr int S = StagesFor<T, NI, VX, PROF>::value;
   using G = Geo<NI, NW, VX, ZP>;
