@@ -256,8 +256,11 @@ int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  p.rc = 64;
-  for (int64_t rc = 256; rc >= 128; rc >>= 1) {
+#ifndef DPM_M2_MIN_RC
+#define DPM_M2_MIN_RC 16   // small images: shorter row chunks, more CTAs in flight (cfg1 graph 22.9 -> 18.8 us)
+#endif
+  p.rc = DPM_M2_MIN_RC;
+  for (int64_t rc = 256; rc > DPM_M2_MIN_RC; rc >>= 1) {
     int64_t nb = 0;
     for (int k = 0; k < s.n_img; ++k) nb += ((s.W[k] + M2_THREADS - 1) / M2_THREADS) * ((s.H[k] + rc - 1) / rc);
     if (nb * B >= 8 * (int64_t)sms) { p.rc = rc; break; }
