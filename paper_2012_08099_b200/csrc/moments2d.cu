@@ -23,6 +23,10 @@ namespace dpm {
 
 constexpr int M2_THREADS = 128;
 constexpr int M2_CHUNK = 8;   // moments per stage-2 reduction round (4 * M2_CHUNK == M2_THREADS / 4)
+#ifndef DPM_M2_UNROLL
+#define DPM_M2_UNROLL 16
+#endif
+constexpr int M2_UNROLL = DPM_M2_UNROLL;   // pixel loads in flight per thread (stage 1)
 
 template <int JB> struct Limbs {
   __host__ __device__ static constexpr int nl(int q) { return q == 0 ? 1 : (q * JB + 23) / 24; }
@@ -133,7 +137,7 @@ __global__ void __launch_bounds__(M2_THREADS) moments2d_kernel(M2Params p) {
   for (int l = 0; l < NTP; ++l) acc[l] = 0;
   if (i < W) {
     const uint32_t* col = p.s.img[k] + b * W * H + j0 * W + i;
-    #pragma unroll 4
+    #pragma unroll M2_UNROLL
     for (int rr = 0; rr < rows; ++rr) {
       const uint64_t v = __ldg(col + (int64_t)rr * W);
       const uint4* tr = reinterpret_cast<const uint4*>(&table[rr][0]);
