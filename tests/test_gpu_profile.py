@@ -37,6 +37,7 @@ SHAPES = [
     ((100, 17, 256), np.uint16),    # two z-tiles
     ((16, 8, 64), np.uint8),        # VX = 4 (16 planes per warp, 2 CTAs per SM at order 3)
     ((150, 9, 264), np.uint8),      # VX = 8 uint8 (16 planes per warp at orders 3-4), two z-tiles
+    ((140, 10, 128), np.uint16),    # VX = 4 uint16 (16 planes / 2 CTAs at order 3), two z-tiles
     ((9, 7, 5), np.uint8),          # generic kernel
     ((13, 11, 203), np.uint16),     # generic kernel (unaligned rows)
 ]
