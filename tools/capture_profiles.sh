@@ -8,7 +8,7 @@ TAG=${1:-r01}
 CFG=${2:-5}
 mkdir -p gpurun_out
 timeout 900 python bench.py --config "$CFG" --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > "gpurun_out/${TAG}_bench.json"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"project_stream|project_generic|moments2d|derive3d|Fill" -c 400 --csv \
   --log-file "gpurun_out/${TAG}_launches.csv" \
   python bench.py --config "$CFG" --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > "gpurun_out/${TAG}_ncu_launches.log" 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:project_stream -s 1 -c 1 \
