@@ -354,7 +354,7 @@ struct RegionCol {
 template <typename T, int NI, int NW, int VX, int STAGES, bool PROF, int ZP, int CTAS>
 __global__ void __launch_bounds__(32 * NW, CTAS)
 project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
-  static_assert(ZP == 8 || (ZP == 16 && PROF && NI <= 5), "16-plane warps: profile mode, orders <= 4");
+  static_assert(ZP == 8 || ((ZP == 16 || ZP == 32) && PROF && NI <= 5), "16/32-plane warps: profile mode, orders <= 4");
   using G = Geo<NI, NW, VX, ZP>;
   using V = typename Vec<T, VX>::type;
   constexpr int SX = G::SX, SZ = G::SZ, THREADS = G::THREADS;
@@ -745,7 +745,7 @@ size_t project_stream_workspace(const dpm_volume_desc*, int) { return 0; }
 // of orders >= 5 need more registers (then 8 warps, <= 255 registers); the
 // 4-wide lanes of order 3 fit 128 registers, so 16 warps (128-plane z-tiles)
 #ifndef DPM_BATCH_ZP
-#define DPM_BATCH_ZP 16  // planes per warp of the 4-wide-lane order-3 profile variant: 16 = 8 warps x 2 CTAs/SM (v27)
+#define DPM_BATCH_ZP 32  // planes per warp of the 4-wide-lane order-3 profile variant: 32 = 4 warps x 4 CTAs/SM (v27, v29)
 #endif
 // 8-wide uint8 lanes at orders 3-4 likewise (16 planes, 6 warps x 2 CTAs/SM:
 // 1024^3 u8 K3 -3 %); for uint16 the 2-CTA shared-memory budget leaves 1-2
@@ -754,11 +754,12 @@ size_t project_stream_workspace(const dpm_volume_desc*, int) { return 0; }
 #define DPM_WIDE_ZP 16
 #endif
 template <typename T, int NI, int VX, bool PROF> struct CfgFor {
-  static constexpr bool batch16 = DPM_BATCH_ZP == 16 && VX == 4 && NI == 4 && PROF;
+  static constexpr bool batch16 = DPM_BATCH_ZP >= 16 && VX == 4 && NI == 4 && PROF;
   static constexpr bool wide16 = DPM_WIDE_ZP == 16 && VX == 8 && NI <= 5 && PROF && sizeof(T) == 1;
-  static constexpr int ZP = (batch16 || wide16) ? 16 : 8;
-  static constexpr int CTAS = (batch16 || wide16) ? 2 : 1;
-  static constexpr int NW = batch16 ? 8 : wide16 ? 6 : (VX == 4 && NI == 4) ? 16 : 12;
+  // batch layout: z-tile 128 = NW x ZP, 16 warps per SM over 16 / NW CTAs
+  static constexpr int ZP = batch16 ? DPM_BATCH_ZP : wide16 ? 16 : 8;
+  static constexpr int NW = batch16 ? 128 / DPM_BATCH_ZP : wide16 ? 6 : (VX == 4 && NI == 4) ? 16 : 12;
+  static constexpr int CTAS = batch16 ? 16 / NW : wide16 ? 2 : 1;
 };
 
 // stages: as many 4-D boxes as fit next to the row buffers
@@ -768,7 +769,7 @@ template <typename T, int NI, int VX, bool PROF> struct StagesFor {
   using GG = Geo<NI, NW, VX, C::ZP>;
   static constexpr int BOX = 32 * VX * C::ZP * NW * (int)sizeof(T);
   static constexpr int ROWS = 2 * GG::WORDS * 4 + 2 * GG::YZT * 4 + (PROF ? GG::PW * 4 : 0);
-  static constexpr int FIT = ((C::CTAS == 1 ? 220 : 111) * 1024 - ROWS) / BOX;
+  static constexpr int FIT = ((C::CTAS == 1 ? 220 : 222 / C::CTAS) * 1024 - ROWS) / BOX;
   static constexpr int value = FIT > 12 ? 12 : FIT;
 };
 
@@ -780,7 +781,7 @@ static int launch_one(const dpm_volume_desc* d, const void* vox, int grid, cudaS
   using G = Geo<NI, NW, VX, ZP>;
   constexpr size_t bytes = (size_t)S * G::SX * G::SZ * sizeof(T) + 2 * G::WORDS * 4 + 2 * G::YZT * 4 + S * 8 + 64 + 160 +
                            (PROF ? G::PW * 4 : 0);
-  static_assert(bytes <= (CTAS == 1 ? 227 : 112) * 1024, "shared memory budget");
+  static_assert(bytes <= (CTAS == 1 ? 227 : 224 / CTAS) * 1024, "shared memory budget");
   const int64_t es = sizeof(T);
   CUtensorMap map;
   const cuuint64_t dims[4] = {(cuuint64_t)d->L, (cuuint64_t)d->M, (cuuint64_t)d->N, (cuuint64_t)d->B};
