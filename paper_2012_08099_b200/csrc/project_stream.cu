@@ -757,8 +757,10 @@ template <typename T, int NI, int VX, bool PROF> struct CfgFor {
   static constexpr bool batch16 = DPM_BATCH_ZP >= 16 && VX == 4 && NI == 4 && PROF;
   static constexpr bool wide16 = DPM_WIDE_ZP == 16 && VX == 8 && NI <= 5 && PROF && sizeof(T) == 1;
   // batch layout: z-tile 128 = NW x ZP, 16 warps per SM over 16 / NW CTAs
-  static constexpr int ZP = batch16 ? DPM_BATCH_ZP : wide16 ? 16 : 8;
-  static constexpr int NW = batch16 ? 128 / DPM_BATCH_ZP : wide16 ? 6 : (VX == 4 && NI == 4) ? 16 : 12;
+  // (16-bit voxels: 16 planes, so a CTA's quarter of shared memory still holds 2+ stages)
+  static constexpr int BZP = sizeof(T) == 1 ? DPM_BATCH_ZP : 16;
+  static constexpr int ZP = batch16 ? BZP : wide16 ? 16 : 8;
+  static constexpr int NW = batch16 ? 128 / BZP : wide16 ? 6 : (VX == 4 && NI == 4) ? 16 : 12;
   static constexpr int CTAS = batch16 ? 16 / NW : wide16 ? 2 : 1;
 };
 
