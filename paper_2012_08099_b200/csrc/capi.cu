@@ -14,6 +14,7 @@ int launch_project_generic(const dpm_volume_desc* d, const void* vox, const Imag
 int launch_project_stream(const dpm_volume_desc* d, const void* vox, const ImageSet& s, unsigned long long* prof,
                           cudaStream_t st, bool* handled);
 int profile_shift(int n_img);
+bool project_stream_single_tile(const dpm_volume_desc* d, const void* vox, int n_img);
 size_t project_stream_workspace(const dpm_volume_desc* d, int n_img);
 int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_t* acc, cudaStream_t st,
                      const M2Extra* ex = nullptr);
@@ -164,14 +165,22 @@ int dpm_profile_layout(const dpm_volume_desc* desc, int order, int64_t* WQ, int6
   return DPM_OK;
 }
 
-// moments-pipeline projection kernel on already zeroed images + profile
+// moments-pipeline projection kernel on a zeroed profile and zeroed images
+// (images_zeroed == false: the caller skipped them because the streaming
+// kernel stores complete rows -- zero them here if it declines)
 static int project_profile_launch(const dpm_volume_desc* desc, const void* d_voxels, int order,
-                                  uint32_t* const* d_images, uint64_t* d_profile, cudaStream_t st) {
+                                  uint32_t* const* d_images, uint64_t* d_profile, cudaStream_t st,
+                                  bool images_zeroed = true) {
   ImageSet s = make_set(desc, num_images(order), d_images, true);
   unsigned long long* prof = reinterpret_cast<unsigned long long*>(d_profile);
   bool handled = false;
   const int rc = launch_project_stream(desc, d_voxels, s, prof, st, &handled);
   if (rc || handled) return rc;
+  if (!images_zeroed)
+    for (int k = 0; k < s.n_img; ++k)
+      if (k != DPM_IMG_ZX &&
+          cudaMemsetAsync(s.img[k], 0, (size_t)(s.W[k] * s.H[k] * desc->B) * sizeof(uint32_t), st) != cudaSuccess)
+        return DPM_ECUDA;
   return launch_project_generic(desc, d_voxels, s, prof, st);
 }
 
@@ -237,10 +246,10 @@ size_t dpm_partial_workspace_bytes(const dpm_volume_desc* desc, int order) {
   return images_bytes(desc, num_images(order), nullptr, true) + align256((size_t)(pg.WQ * desc->B) * sizeof(uint64_t));
 }
 
-// acc_adjacent: d_acc is the acc_bytes_of() bytes right before d_ws (dpm_moments'
-// own workspace carve), so one memset zeroes accumulator, images and profile
-// fused (dpm_moments): the volume counters follow the partial scratch in the
-// same workspace, and the moments launch ends with the epilogue
+// fused (dpm_moments): the workspace is [images | profile | counters | acc]
+// (acc_adjacent: d_acc directly follows the counters), and the moments launch
+// ends with the epilogue; the profile, counters and accumulator are then one
+// contiguous range to zero
 static int moments_partial_impl(const dpm_volume_desc* desc, const void* d_voxels, int order, void* d_ws,
                                 size_t ws_bytes, uint64_t* d_acc, void* stream, bool acc_adjacent,
                                 const FusedOut* fused = nullptr) {
@@ -258,15 +267,18 @@ static int moments_partial_impl(const dpm_volume_desc* desc, const void* d_voxel
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // one zeroing of the contiguous images + profile scratch, one of the accumulator
   // (or none when the caller's accumulator directly precedes it: dpm_moments)
-  char* z0 = acc_adjacent ? reinterpret_cast<char*>(d_acc) : base;
-  const size_t zb = dpm_partial_workspace_bytes(desc, order) + (acc_adjacent ? acc_bytes_of(desc, order) : 0) +
-                    (fused ? align256((size_t)desc->B * sizeof(unsigned int)) : 0);
+  // (single-tile volumes: the images are stored whole by the kernel, zero only the profile and counters)
+  const bool single = project_stream_single_tile(desc, d_voxels, n_img);
+  const size_t tail = dpm_partial_workspace_bytes(desc, order) - ib +
+                      (fused ? align256((size_t)desc->B * sizeof(unsigned int)) : 0);
+  char* z0 = single ? reinterpret_cast<char*>(prof) : base;
+  const size_t zb = (single ? 0 : ib) + tail + (acc_adjacent ? acc_bytes_of(desc, order) : 0);
   if (cudaMemsetAsync(z0, 0, zb, st) != cudaSuccess) return DPM_ECUDA;
   if (!acc_adjacent &&
       cudaMemsetAsync(d_acc, 0, (size_t)(desc->B * n_img * n2d(order) * 4) * sizeof(uint64_t), st) != cudaSuccess)
     return DPM_ECUDA;
   reset_launches();
-  rc = project_profile_launch(desc, d_voxels, order, imgs, prof, st);
+  rc = project_profile_launch(desc, d_voxels, order, imgs, prof, st, !single);
   if (rc) return rc;
   return moments2d_profile_launch(desc, order, imgs, prof, d_acc, st, fused);
 }
@@ -348,17 +360,18 @@ int dpm_moments(const dpm_volume_desc* desc, const void* d_voxels, int order, vo
   if (rc) return rc;
   if (check_order(order) || !d_voxels || !d_m3d_i128 || !d_status) return DPM_EINVAL;
   if (ws_bytes < dpm_workspace_bytes(desc, order) || !d_ws) return DPM_EWORKSPACE;
-  uint64_t* acc = static_cast<uint64_t*>(d_ws);
-  const size_t acc_bytes = acc_bytes_of(desc, order);
-  char* pws = static_cast<char*>(d_ws) + acc_bytes;
+  // workspace: [images | profile | counters | acc]
+  char* pws = static_cast<char*>(d_ws);
   const size_t pbytes = dpm_partial_workspace_bytes(desc, order);
+  const size_t cbytes = align256((size_t)desc->B * sizeof(unsigned int));
+  uint64_t* acc = reinterpret_cast<uint64_t*>(pws + pbytes + cbytes);
   FusedOut f;
   f.cnt = reinterpret_cast<unsigned int*>(pws + pbytes);
   f.i128 = d_m3d_i128;
   f.f64 = d_m3d_f64;
   f.status = d_status;
   // memset, projection pass, one moments launch that ends with the epilogue
-  return moments_partial_impl(desc, d_voxels, order, pws, ws_bytes - acc_bytes, acc, stream, true, &f);
+  return moments_partial_impl(desc, d_voxels, order, pws, pbytes, acc, stream, true, &f);
 }
 
 int dpm_acc_add(uint64_t* d_acc_out, const uint64_t* d_acc_in, int64_t count, void* stream);

@@ -66,6 +66,10 @@ namespace dpm {
 #define DPM_FMA_FOLDS 16
 #endif
 // DPM_UNPACK_MIX: 16-bit unpack as hi = SHF (ALU), lo = IMAD (FMA) instead of LOP3 + SHF
+// single-tile volumes store complete image rows instead of adding them
+#ifndef DPM_SINGLE_TILE
+#define DPM_SINGLE_TILE 1
+#endif
 #ifndef DPM_UNPACK_MIX
 #define DPM_UNPACK_MIX 0
 #endif
@@ -81,6 +85,10 @@ struct StreamParams {
   // the ZX image; qoff = |t| (N - 1) for t < 0, else 0
   unsigned long long* prof;
   int64_t WQ, qoff;
+  // single-tile moments pass (one x-tile and one z-tile per volume): every image
+  // row is completed by the one CTA that owns its row-step, so rows are stored
+  // (no zeroing, no read-modify-write in L2) instead of added
+  uint32_t single;
 };
 
 // Profile direction t of the moments pass (x + t z, summed over y), by image
@@ -307,7 +315,7 @@ struct ColGeom {
 // global row; [lo, hi) is the part of the padded extent inside the row.
 // Cells past NCELL are never written (zero), so reducing them is harmless.
 template <int VX, int S, int NCELL, int THREADS>
-__device__ __forceinline__ void flush_region(uint32_t* rw, int tid, uint32_t* g, int lo, int hi) {
+__device__ __forceinline__ void flush_region(uint32_t* rw, int tid, uint32_t* g, int lo, int hi, bool single) {
   constexpr int WORDS = (NCELL + VX - 1) / VX;
   constexpr int QCH = (WORDS + 3) / 4;
   constexpr int NCH = VX * QCH;
@@ -323,7 +331,12 @@ __device__ __forceinline__ void flush_region(uint32_t* rw, int tid, uint32_t* g,
     *wp = make_uint4(0u, 0u, 0u, 0u);
     const int c0 = VX * q + r;
     uint32_t* gp = g + c0;
-    if (interior) {
+    if (single) {
+      ptx::st_global_if(gp, v.x, c0 >= lo && c0 < hi);
+      ptx::st_global_if(gp + VX, v.y, c0 + VX >= lo && c0 + VX < hi);
+      ptx::st_global_if(gp + 2 * VX, v.z, c0 + 2 * VX >= lo && c0 + 2 * VX < hi);
+      ptx::st_global_if(gp + 3 * VX, v.w, c0 + 3 * VX >= lo && c0 + 3 * VX < hi);
+    } else if (interior) {
       ptx::red_global_add_off<0>(gp, v.x);
       ptx::red_global_add_off<4 * VX>(gp, v.y);
       ptx::red_global_add_off<8 * VX>(gp, v.z);
@@ -380,6 +393,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
   uint64_t* full = reinterpret_cast<uint64_t*>(yzb + 2 * YZT);                  // [STAGES]
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t rows_addr = ptx::smem_addr(rows), full_addr = ptx::smem_addr(full);
+  const bool single = PROF && p.single != 0;
 
   for (int i = tid; i < 2 * G::WORDS + 2 * YZT; i += THREADS) rows[i] = 0;
   if constexpr (PROF) {
@@ -618,7 +632,8 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
     if (YZT > 0) {
       if (lane < ZP) yzb[yzpar * SZ * 8 + (ZP * w + lane) * 8 + (y & 7)] = yzmine;
     } else {
-      ptx::red_global_add_if(yz_col + y, yzmine, lane < ZP && yzmine != 0 && lane < g.zc);
+      if (single) ptx::st_global_if(yz_col + y, yzmine, lane < ZP && lane < g.zc);
+      else ptx::red_global_add_if(yz_col + y, yzmine, lane < ZP && yzmine != 0 && lane < g.zc);
     }
 
     // ---- add the XY column sums and the oblique windows to the CTA rows
@@ -672,16 +687,16 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
       const uint32_t rowid = (uint32_t)g.b * (uint32_t)p.M + (uint32_t)y;
       auto row = [&](int k, uint32_t w32, int64_t g0) { return p.s.img[k] + ((uint64_t)rowid * w32 + g0); };
       const RegionCol* rc = rcs + 5 * rslot;   // written before this column's first barrier
-      flush_region<VX, G::SXY, SX, THREADS>(rw + G::XY, tid, row(DPM_IMG_XY, (uint32_t)p.L, rc[0].g0), rc[0].lo, rc[0].hi);
+      flush_region<VX, G::SXY, SX, THREADS>(rw + G::XY, tid, row(DPM_IMG_XY, (uint32_t)p.L, rc[0].g0), rc[0].lo, rc[0].hi, single);
       const uint32_t Wd = (uint32_t)p.s.W[DPM_IMG_DIAG];
-      flush_region<VX, G::SOB, G::W1, THREADS>(rw + G::DG, tid, row(DPM_IMG_DIAG, Wd, rc[1].g0), rc[1].lo, rc[1].hi);
+      flush_region<VX, G::SOB, G::W1, THREADS>(rw + G::DG, tid, row(DPM_IMG_DIAG, Wd, rc[1].g0), rc[1].lo, rc[1].hi, single);
       if (NI > DPM_IMG_ANTI)
-        flush_region<VX, G::SOB, G::W1, THREADS>(rw + G::AN, tid, row(DPM_IMG_ANTI, Wd, rc[2].g0), rc[2].lo, rc[2].hi);
+        flush_region<VX, G::SOB, G::W1, THREADS>(rw + G::AN, tid, row(DPM_IMG_ANTI, Wd, rc[2].g0), rc[2].lo, rc[2].hi, single);
       if (NI > DPM_IMG_X2P) {
         const uint32_t W2g = (uint32_t)p.s.W[DPM_IMG_X2P];
-        flush_region<VX, G::SOB, G::W2, THREADS>(rw + G::XP, tid, row(DPM_IMG_X2P, W2g, rc[3].g0), rc[3].lo, rc[3].hi);
+        flush_region<VX, G::SOB, G::W2, THREADS>(rw + G::XP, tid, row(DPM_IMG_X2P, W2g, rc[3].g0), rc[3].lo, rc[3].hi, single);
         if (NI > DPM_IMG_X2M)
-          flush_region<VX, G::SOB, G::W2, THREADS>(rw + G::XM, tid, row(DPM_IMG_X2M, W2g, rc[4].g0), rc[4].lo, rc[4].hi);
+          flush_region<VX, G::SOB, G::W2, THREADS>(rw + G::XM, tid, row(DPM_IMG_X2M, W2g, rc[4].g0), rc[4].lo, rc[4].hi, single);
       }
     }
     parity ^= 1;
@@ -698,7 +713,13 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
         if ((SZ * 8) % THREADS != 0 && i >= SZ * 8) break;
         const uint32_t v = tb[i];
         tb[i] = 0;
-        ptx::red_global_add_if(gy + (int64_t)(i >> 3) * p.M + (i & 7), v, v != 0);
+        if (single) {   // only this run's rows of the group, only planes inside the volume
+          const int32_t yy = (y & ~7) + (i & 7);
+          ptx::st_global_if(gy + (int64_t)(i >> 3) * p.M + (i & 7), v,
+                            yy >= y_first && yy <= y && g.Z0 + (i >> 3) < p.N);
+        } else {
+          ptx::red_global_add_if(gy + (int64_t)(i >> 3) * p.M + (i & 7), v, v != 0);
+        }
       }
       yzpar ^= 1;
     }
@@ -753,8 +774,10 @@ size_t project_stream_workspace(const dpm_volume_desc*, int) { return 0; }
 #ifndef DPM_WIDE_ZP
 #define DPM_WIDE_ZP 16
 #endif
-template <typename T, int NI, int VX, bool PROF> struct CfgFor {
-  static constexpr bool batch16 = DPM_BATCH_ZP >= 16 && VX == 4 && NI == 4 && PROF;
+// SMALL: few row-steps in total (tiny volumes): the latency of one row-step
+// dominates, so 8 planes per warp (16 warps, 1 CTA) beats the batch layout
+template <typename T, int NI, int VX, bool PROF, bool SMALL = false> struct CfgFor {
+  static constexpr bool batch16 = DPM_BATCH_ZP >= 16 && VX == 4 && NI == 4 && PROF && !SMALL;
   static constexpr bool wide16 = DPM_WIDE_ZP == 16 && VX == 8 && NI <= 5 && PROF && sizeof(T) == 1;
   // batch layout: z-tile 128 = NW x ZP, 16 warps per SM over 16 / NW CTAs
   // (16-bit voxels: 16 planes, so a CTA's quarter of shared memory still holds 2+ stages)
@@ -765,8 +788,8 @@ template <typename T, int NI, int VX, bool PROF> struct CfgFor {
 };
 
 // stages: as many 4-D boxes as fit next to the row buffers
-template <typename T, int NI, int VX, bool PROF> struct StagesFor {
-  using C = CfgFor<T, NI, VX, PROF>;
+template <typename T, int NI, int VX, bool PROF, bool SMALL = false> struct StagesFor {
+  using C = CfgFor<T, NI, VX, PROF, SMALL>;
   static constexpr int NW = C::NW;
   using GG = Geo<NI, NW, VX, C::ZP>;
   static constexpr int BOX = 32 * VX * C::ZP * NW * (int)sizeof(T);
@@ -775,11 +798,11 @@ template <typename T, int NI, int VX, bool PROF> struct StagesFor {
   static constexpr int value = FIT > 12 ? 12 : FIT;
 };
 
-template <typename T, int NI, int VX, bool PROF>
+template <typename T, int NI, int VX, bool PROF, bool SMALL = false>
 static int launch_one(const dpm_volume_desc* d, const void* vox, int grid, cudaStream_t st, StreamParams p) {
-  using C = CfgFor<T, NI, VX, PROF>;
+  using C = CfgFor<T, NI, VX, PROF, SMALL>;
   constexpr int NW = C::NW, ZP = C::ZP, CTAS = C::CTAS;
-  constexpr int S = StagesFor<T, NI, VX, PROF>::value;
+  constexpr int S = StagesFor<T, NI, VX, PROF, SMALL>::value;
   using G = Geo<NI, NW, VX, ZP>;
   constexpr size_t bytes = (size_t)S * G::SX * G::SZ * sizeof(T) + 2 * G::WORDS * 4 + 2 * G::YZT * 4 + S * 8 + 64 + 160 +
                            (PROF ? G::PW * 4 : 0);
@@ -803,6 +826,7 @@ static int launch_one(const dpm_volume_desc* d, const void* vox, int grid, cudaS
   p.ntx = (d->L + G::SX - 1) / G::SX;
   p.ntz = (d->N + G::SZ - 1) / G::SZ;
   p.ncol = p.ntx * p.ntz * d->B;
+  p.single = (DPM_SINGLE_TILE && PROF && p.ntx == 1 && p.ntz == 1) ? 1u : 0u;
   static std::once_flag once;
   std::call_once(once, [] {
     cudaFuncSetAttribute(project_stream_kernel<T, NI, NW, VX, S, PROF, ZP, CTAS>,
@@ -827,6 +851,12 @@ static int launch_typed(int n_img, const dpm_volume_desc* d, const void* vox, in
 template <typename T>
 static int launch_vx(int n_img, const dpm_volume_desc* d, const void* vox, int grid, cudaStream_t st,
                      const StreamParams& p) {
+  if (p.prof && n_img == 4 && lane_width(d) == 4) {
+    // batch layout (32 planes per warp, 4 CTAs per SM) unless the whole pass is
+    // only a few row-steps (cfg1: 64), where per-row-step latency dominates
+    const int64_t rowsteps = ((d->L + 127) / 128) * ((d->N + 127) / 128) * d->B * d->M;
+    if (rowsteps < 8 * (int64_t)grid) return launch_one<T, 4, 4, true, true>(d, vox, grid, st, p);
+  }
   if (p.prof)
     return lane_width(d) == 8 ? launch_typed<T, 8, true>(n_img, d, vox, grid, st, p)
                               : launch_typed<T, 4, true>(n_img, d, vox, grid, st, p);
@@ -839,6 +869,28 @@ int profile_shift(int n_img) {
 }
 
 bool project_stream_eligible(const dpm_volume_desc* d, const void* vox) { return stream_eligible(d, vox); }
+
+template <typename T, int VX> static int64_t ztile_for(int n_img) {
+  switch (n_img) {
+    case 4: return (int64_t)CfgFor<T, 4, VX, true>::ZP * CfgFor<T, 4, VX, true>::NW;
+    case 5: return (int64_t)CfgFor<T, 5, VX, true>::ZP * CfgFor<T, 5, VX, true>::NW;
+    case 6: return (int64_t)CfgFor<T, 6, VX, true>::ZP * CfgFor<T, 6, VX, true>::NW;
+    default: return (int64_t)CfgFor<T, 7, VX, true>::ZP * CfgFor<T, 7, VX, true>::NW;
+  }
+}
+
+// true when the moments pass will run the streaming kernel with ONE x-tile and
+// ONE z-tile per volume: it then stores complete image rows (p.single), and the
+// caller need not zero the images
+bool project_stream_single_tile(const dpm_volume_desc* d, const void* vox, int n_img) {
+  if (!DPM_SINGLE_TILE || n_img < 4 || !stream_eligible(d, vox)) return false;
+  const int vx = lane_width(d);
+  int64_t sz;
+  if (d->dtype == DPM_U8) sz = vx == 8 ? ztile_for<uint8_t, 8>(n_img) : ztile_for<uint8_t, 4>(n_img);
+  else if (d->dtype == DPM_U16) sz = vx == 8 ? ztile_for<uint16_t, 8>(n_img) : ztile_for<uint16_t, 4>(n_img);
+  else sz = vx == 8 ? ztile_for<int16_t, 8>(n_img) : ztile_for<int16_t, 4>(n_img);
+  return d->L <= 32 * vx && d->N <= sz;
+}
 
 // prof != nullptr: moments mode (images except ZX + the profile along x + t z
 // summed over y, t = profile_shift(n_img)); the caller zeroed images and profile

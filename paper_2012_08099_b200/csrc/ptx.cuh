@@ -226,5 +226,18 @@ template <int OFF>
 __device__ __forceinline__ void red_global_add_off(uint32_t* gptr, uint32_t v) {
   asm volatile("red.global.add.u32 [%0+%1], %2;" ::"l"(gptr), "n"(OFF), "r"(v) : "memory");
 }
+// st.global.u32 [gptr + OFF] (rows a single CTA completes: no read-modify-write)
+template <int OFF>
+__device__ __forceinline__ void st_global_off(uint32_t* gptr, uint32_t v) {
+  asm volatile("st.global.u32 [%0+%1], %2;" ::"l"(gptr), "n"(OFF), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_global_if(uint32_t* gptr, uint32_t v, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.u32 p, %2, 0;\n\t"
+      "@p st.global.u32 [%0], %1;\n\t}" ::"l"(gptr),
+      "r"(v), "r"((uint32_t)pred)
+      : "memory");
+}
 }  // namespace ptx
 }  // namespace dpm

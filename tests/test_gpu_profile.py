@@ -40,6 +40,8 @@ SHAPES = [
     ((140, 10, 128), np.uint16),    # VX = 4 uint16 (16 planes / 2 CTAs at order 3), two z-tiles
     ((9, 7, 5), np.uint8),          # generic kernel
     ((13, 11, 203), np.uint16),     # generic kernel (unaligned rows)
+    ((60, 300, 128), np.uint8),     # single tile (rows stored, images not zeroed), runs not aligned to 8 rows
+    ((50, 200, 256), np.uint16),    # single tile with 8-wide lanes, all orders (order 6: direct YZ stores)
 ]
 
 
