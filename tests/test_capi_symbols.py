@@ -67,3 +67,13 @@ def test_invalid_arguments_rejected_without_a_device():
     with pytest.raises(OverflowError):
         nat.check(nat.DPM_EOVERFLOW, "x")
     assert np.int64  # numpy import used
+
+
+def test_envelope_order6_profile_rule():
+    """Order 6 adds mass * max(L,M,N)^6 < 2^116 (the profile solve)
+    on top of the 2^126 image envelope: this shape passes the latter, not the former."""
+    lib = nat.lib()
+    n = 4096
+    assert lib.dpm_check_envelope(n, n, n, 257, 5) == nat.DPM_OK        # images + profile solve fine at order 5
+    assert lib.dpm_check_envelope(n, n, n, 257, 6) == nat.DPM_EOVERFLOW
+    assert lib.dpm_check_envelope(n, n, n, 255, 6) == nat.DPM_OK        # just below 2^116
