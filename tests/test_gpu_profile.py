@@ -116,3 +116,14 @@ def test_profile_graphed_stages_launches():
     slab = torch.from_numpy(rng.integers(0, 65535, size=(24, 24, 264)).astype(np.uint16)).cuda()
     st = engine.GraphedSlabStages(slab, 6, z0=16)
     assert st.launches == 3      # projection, image + profile moments (one launch), epilogue
+
+
+@pytest.mark.parametrize("order", [4, 6])
+def test_profile_batch_multi_tile(order):
+    """Batch of volumes that need several x-tiles and z-tiles each (atomic rows,
+    per-volume profiles and counters)."""
+    rng = np.random.default_rng(order + 40)
+    vols = rng.integers(0, 65536, size=(3, 100, 6, 264)).astype(np.uint16)
+    got = vm.dpm_moments_batch(vols, order)
+    for b in range(3):
+        assert got[b].values == oracle.naive(vols[b], order)
