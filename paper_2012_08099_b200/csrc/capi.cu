@@ -15,6 +15,9 @@ int launch_project_stream(const dpm_volume_desc* d, const void* vox, const Image
                           cudaStream_t st, bool* handled);
 int profile_shift(int n_img);
 bool project_stream_single_tile(const dpm_volume_desc* d, const void* vox, int n_img);
+bool project_stream_eligible(const dpm_volume_desc* d, const void* vox);
+int launch_pad_copy(const dpm_volume_desc* d, const void* vox, int64_t z, int64_t n, int64_t Lp, void* dst,
+                    cudaStream_t st);
 size_t project_stream_workspace(const dpm_volume_desc* d, int n_img);
 int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_t* acc, cudaStream_t st,
                      const M2Extra* ex = nullptr);
@@ -252,7 +255,7 @@ size_t dpm_partial_workspace_bytes(const dpm_volume_desc* desc, int order) {
 // contiguous range to zero
 static int moments_partial_impl(const dpm_volume_desc* desc, const void* d_voxels, int order, void* d_ws,
                                 size_t ws_bytes, uint64_t* d_acc, void* stream, bool acc_adjacent,
-                                const FusedOut* fused = nullptr) {
+                                const FusedOut* fused = nullptr, bool zero_acc = true) {
   int rc = check_desc(desc);
   if (rc) return rc;
   if (check_order(order) || !d_voxels || !d_acc) return DPM_EINVAL;
@@ -274,7 +277,7 @@ static int moments_partial_impl(const dpm_volume_desc* desc, const void* d_voxel
   char* z0 = single ? reinterpret_cast<char*>(prof) : base;
   const size_t zb = (single ? 0 : ib) + tail + (acc_adjacent ? acc_bytes_of(desc, order) : 0);
   if (cudaMemsetAsync(z0, 0, zb, st) != cudaSuccess) return DPM_ECUDA;
-  if (!acc_adjacent &&
+  if (!acc_adjacent && zero_acc &&
       cudaMemsetAsync(d_acc, 0, (size_t)(desc->B * n_img * n2d(order) * 4) * sizeof(uint64_t), st) != cudaSuccess)
     return DPM_ECUDA;
   reset_launches();
@@ -328,11 +331,90 @@ int dpm_derive3d(const dpm_volume_desc* desc, const uint64_t* d_acc, int order, 
                          static_cast<cudaStream_t>(stream));
 }
 
+// Staged moments pass for single volumes the streaming (TMA) kernel cannot
+// read in place -- row pitch not a multiple of 16 bytes, width not a multiple
+// of the lane width (e.g. the odd cube sides of the reference's bench sweep):
+// z-slabs are copied into a zero-padded pitched scratch (int16 + offset is
+// converted to uint16 on the way), each slab runs the streaming moments pass
+// in global coordinates into one accumulator, and the epilogue runs once.
+// The padding columns are zero, so images are only wider, moments identical.
+struct Staged {
+  bool use;
+  int64_t Lp, S;            // padded width, planes per slab
+  dpm_volume_desc slab;     // geometry of a full slab (N = S)
+};
+static constexpr size_t kStagedSlabBytes = size_t(256) << 20;   // scratch budget per slab
+static Staged staged_plan(const dpm_volume_desc* d) {
+  Staged g;
+  memset(&g, 0, sizeof(g));
+  if (d->B != 1 || d->L < 32 || d->N < 8) return g;        // tiny / batched: the generic kernel
+  const int64_t es_out = d->dtype == DPM_U8 ? 1 : 2;
+  const int64_t es_in = d->dtype == DPM_U8 ? 1 : 2;
+  const bool pitch_ok = (d->stride_y * es_in) % 16 == 0 && (d->stride_z * es_in) % 16 == 0;
+  const int64_t lw = d->L > 128 ? 8 : 4;
+  if (pitch_ok && d->L % lw == 0) return g;                  // the streaming kernel reads it in place
+  const int64_t a = 16 / es_out;                             // pitch multiple (elements)
+  g.Lp = (d->L + a - 1) / a * a;
+  const int64_t plane = g.Lp * d->M * es_out;
+  int64_t S = (int64_t)(kStagedSlabBytes / (size_t)plane);
+  if (S >= 96) S = S / 96 * 96;                              // whole z-tiles of the streaming kernel
+  S = imax64(8, imin64(S, d->N));
+  g.S = S;
+  g.slab = *d;
+  g.slab.L = g.Lp;
+  g.slab.N = S;
+  g.slab.B = 1;
+  g.slab.stride_y = g.Lp;
+  g.slab.stride_z = g.Lp * d->M;
+  g.slab.stride_b = g.Lp * d->M * S;
+  g.slab.dtype = d->dtype == DPM_U8 ? DPM_U8 : DPM_U16;
+  g.slab.offset = 0;
+  g.use = true;
+  return g;
+}
+
 size_t dpm_workspace_bytes(const dpm_volume_desc* desc, int order) {
   if (check_desc(desc) || check_order(order)) return 0;
   const int n_img = num_images(order);
-  return align256((size_t)(desc->B * n_img * n2d(order) * 4) * sizeof(uint64_t)) +
-         dpm_partial_workspace_bytes(desc, order) + align256((size_t)desc->B * sizeof(unsigned int));
+  const size_t base = align256((size_t)(desc->B * n_img * n2d(order) * 4) * sizeof(uint64_t)) +
+                      dpm_partial_workspace_bytes(desc, order) + align256((size_t)desc->B * sizeof(unsigned int));
+  const Staged g = staged_plan(desc);
+  if (!g.use) return base;
+  const int64_t es_out = g.slab.dtype == DPM_U8 ? 1 : 2;
+  const size_t staged = align256((size_t)(n_img * n2d(order) * 4) * sizeof(uint64_t)) +
+                        dpm_partial_workspace_bytes(&g.slab, order) +
+                        align256((size_t)(g.Lp * desc->M * g.S * es_out));
+  return base > staged ? base : staged;
+}
+
+static int moments_staged(const dpm_volume_desc* desc, const Staged& g, const void* d_voxels, int order, void* d_ws,
+                          int64_t* d_m3d_i128, double* d_m3d_f64, int32_t* d_status, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int n_img = num_images(order);
+  // workspace: [acc | slab images + profile | scratch]
+  char* base = static_cast<char*>(d_ws);
+  uint64_t* acc = reinterpret_cast<uint64_t*>(base);
+  const size_t acc_bytes = align256((size_t)(n_img * n2d(order) * 4) * sizeof(uint64_t));
+  char* pws = base + acc_bytes;
+  const size_t pbytes = dpm_partial_workspace_bytes(&g.slab, order);
+  char* scratch = pws + pbytes;
+  if (cudaMemsetAsync(acc, 0, acc_bytes, st) != cudaSuccess) return DPM_ECUDA;
+  int launches = 0;
+  for (int64_t z = 0; z < desc->N; z += g.S) {
+    dpm_volume_desc sd = g.slab;
+    sd.N = imin64(g.S, desc->N - z);
+    sd.stride_b = g.Lp * desc->M * sd.N;
+    sd.z0 = desc->z0 + z;
+    int rc = launch_pad_copy(desc, d_voxels, z, sd.N, g.Lp, scratch, st);
+    if (rc) return rc;
+    launches += 1;
+    rc = moments_partial_impl(&sd, scratch, order, pws, pbytes, acc, stream, false, nullptr, false);
+    launches += dpm_last_launch_count();
+    if (rc) return rc;
+  }
+  const int rc = dpm_derive3d(desc, acc, order, DPM_ACC_PROFILE, d_m3d_i128, d_m3d_f64, d_status, stream);
+  g_launches = launches + dpm_last_launch_count();
+  return rc;
 }
 
 int dpm_check_envelope(int64_t L, int64_t M, int64_t N_global, int64_t vmax, int order) {
@@ -360,6 +442,8 @@ int dpm_moments(const dpm_volume_desc* desc, const void* d_voxels, int order, vo
   if (rc) return rc;
   if (check_order(order) || !d_voxels || !d_m3d_i128 || !d_status) return DPM_EINVAL;
   if (ws_bytes < dpm_workspace_bytes(desc, order) || !d_ws) return DPM_EWORKSPACE;
+  const Staged g = staged_plan(desc);
+  if (g.use) return moments_staged(desc, g, d_voxels, order, d_ws, d_m3d_i128, d_m3d_f64, d_status, stream);
   // workspace: [images | profile | counters | acc]
   char* pws = static_cast<char*>(d_ws);
   const size_t pbytes = dpm_partial_workspace_bytes(desc, order);

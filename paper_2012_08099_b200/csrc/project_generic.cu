@@ -165,4 +165,52 @@ int launch_project_generic(const dpm_volume_desc* d, const void* vox, const Imag
   return DPM_OK;
 }
 
+// ---- staged copies for the moments pass (capi.cu, moments_staged) ----------
+// planes [z, z+n) of one volume -> zero-padded pitched scratch [n][M][Lp]; int16
+// + offset becomes uint16 (the caller guarantees 0..65535), so the slab runs
+// the streaming kernel with offset 0.  One warp per row, coalesced both ways.
+template <typename Tin, typename Tout>
+__global__ void __launch_bounds__(256) pad_copy_kernel(const Tin* src, int64_t sy, int64_t sz, int64_t L, int64_t M,
+                                                       int64_t n, int32_t offset, Tout* dst, int64_t Lp) {
+  const int64_t rows = M * n;
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); r < rows; r += (int64_t)gridDim.x * 8) {
+    const int64_t zz = r / M, yy = r - zz * M;
+    const Tin* s = src + zz * sz + yy * sy;
+    Tout* d = dst + r * Lp;
+    for (int64_t x = lane; x < Lp; x += 32) {
+      uint32_t v = 0;
+      if (x < L) v = (uint32_t)((int32_t)s[x] + offset);
+      d[x] = (Tout)v;
+    }
+  }
+}
+
+int launch_pad_copy(const dpm_volume_desc* d, const void* vox, int64_t z, int64_t n, int64_t Lp, void* dst,
+                    cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t rows = d->M * n;
+  const int grid = (int)imax64(1, imin64((rows + 7) / 8, (int64_t)sms * 16));
+  switch (d->dtype) {
+    case DPM_U8:
+      pad_copy_kernel<uint8_t, uint8_t><<<grid, 256, 0, st>>>(static_cast<const uint8_t*>(vox) + z * d->stride_z,
+                                                            d->stride_y, d->stride_z, d->L, d->M, n, 0,
+                                                            static_cast<uint8_t*>(dst), Lp);
+      break;
+    case DPM_U16:
+      pad_copy_kernel<uint16_t, uint16_t><<<grid, 256, 0, st>>>(static_cast<const uint16_t*>(vox) + z * d->stride_z,
+                                                              d->stride_y, d->stride_z, d->L, d->M, n, 0,
+                                                              static_cast<uint16_t*>(dst), Lp);
+      break;
+    default:
+      pad_copy_kernel<int16_t, uint16_t><<<grid, 256, 0, st>>>(static_cast<const int16_t*>(vox) + z * d->stride_z,
+                                                             d->stride_y, d->stride_z, d->L, d->M, n, d->offset,
+                                                             static_cast<uint16_t*>(dst), Lp);
+  }
+  DPM_CUDA_CHECK_LAUNCH();
+  return DPM_OK;
+}
+
 }  // namespace dpm
