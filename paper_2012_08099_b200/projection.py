@@ -11,6 +11,7 @@ both (L+2N-2) x M -- available through ``project_extended``.
 from __future__ import annotations
 
 import enum
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -101,7 +102,9 @@ def _to_device(volume):
 
     if isinstance(volume, Volume):
         arr = np.ascontiguousarray(volume.voxels)
-        host = torch.from_numpy(arr.copy() if not arr.flags.writeable else arr)
+        with warnings.catch_warnings():   # read-only voxels are only read (copied to the device), never written
+            warnings.simplefilter("ignore", UserWarning)
+            host = torch.from_numpy(arr)
         return host.to("cuda", non_blocking=False)
     if isinstance(volume, torch.Tensor):
         if not volume.is_cuda:
