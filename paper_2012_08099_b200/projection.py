@@ -97,11 +97,76 @@ def _device_images(volume, n_img: int) -> list[np.ndarray]:
     return [t[0].cpu().numpy().view(np.uint32).astype(np.int64) for t in imgs]
 
 
+_TORCH_OF = {}   # numpy dtype -> torch dtype, filled on first use
+
+
+def _torch_dtypes():
+    import torch
+
+    if not _TORCH_OF:
+        _TORCH_OF.update({np.dtype("uint8"): torch.uint8, np.dtype("uint16"): torch.uint16})
+    return _TORCH_OF
+
+
+class _Uploader:
+    """Host -> device copies of large pageable volumes: plane chunks are copied
+    by a thread pool (numpy releases the GIL) into two pinned staging buffers
+    while the other buffer's H2D runs on a copy stream -- ~2-3x the driver's
+    pageable copy rate.  One per process, created lazily."""
+
+    CHUNK = 64 << 20
+    THREADS = 8
+
+    def __init__(self):
+        import torch
+        from concurrent.futures import ThreadPoolExecutor
+
+        self.stage = [torch.empty(self.CHUNK, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        self.done = [torch.cuda.Event() for _ in range(2)]
+        self.stream = torch.cuda.Stream()
+        self.pool = ThreadPoolExecutor(self.THREADS)
+
+    def upload(self, arr: np.ndarray):
+        import torch
+
+        n = arr.shape[0]
+        plane = arr[0].nbytes if n else 1
+        per = max(1, self.CHUNK // plane)
+        if per * plane > self.CHUNK or plane > self.CHUNK:
+            return None                                   # planes larger than a chunk: caller's fallback
+        dev = torch.empty(arr.shape, dtype=_torch_dtypes()[arr.dtype], device="cuda")
+        self.stream.wait_stream(torch.cuda.current_stream())
+        for k, z0 in enumerate(range(0, n, per)):
+            z1 = min(n, z0 + per)
+            i = k % 2
+            self.done[i].synchronize()                    # this staging buffer's previous H2D finished
+            view = self.stage[i][: (z1 - z0) * plane].numpy().view(arr.dtype).reshape((z1 - z0,) + arr.shape[1:])
+            cuts = np.linspace(z0, z1, min(self.THREADS, z1 - z0) + 1).astype(int)
+            list(self.pool.map(lambda ab: np.copyto(view[ab[0] - z0:ab[1] - z0], arr[ab[0]:ab[1]]),
+                               zip(cuts[:-1], cuts[1:])))
+            with torch.cuda.stream(self.stream):
+                dev[z0:z1].copy_(self.stage[i][: (z1 - z0) * plane].view(dev.dtype).view(dev[z0:z1].shape),
+                                 non_blocking=True)
+                self.done[i].record(self.stream)
+        torch.cuda.current_stream().wait_stream(self.stream)
+        return dev
+
+
+_UPLOADER = None
+
+
 def _to_device(volume):
     import torch
 
+    global _UPLOADER
     if isinstance(volume, Volume):
         arr = np.ascontiguousarray(volume.voxels)
+        if arr.nbytes >= (32 << 20) and arr.ndim == 3:
+            if _UPLOADER is None:
+                _UPLOADER = _Uploader()
+            dev = _UPLOADER.upload(arr)
+            if dev is not None:
+                return dev
         with warnings.catch_warnings():   # read-only voxels are only read (copied to the device), never written
             warnings.simplefilter("ignore", UserWarning)
             host = torch.from_numpy(arr)
