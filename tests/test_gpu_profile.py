@@ -156,3 +156,14 @@ def test_staged_multi_slab_equals_padded_in_place():
     padded = np.zeros((600, 500, 1008), dtype=np.uint8)
     padded[:, :, :1001] = vol
     assert got.values == vm.dpm_moments(vm.Volume(padded), 4).values
+
+
+def test_public_api_upload_path_is_exact():
+    """Volumes >= 32 MB reach the device through the pinned, threaded uploader
+    (projection._Uploader): same moments as a direct device tensor."""
+    rng = np.random.default_rng(21)
+    vol = rng.integers(0, 65536, size=(400, 300, 320), dtype=np.uint16)   # 77 MB: two 64 MB staging chunks
+    via_api = vm.dpm_moments(vm.Volume(vol), 6)
+    direct = engine.moments(torch.from_numpy(vol).cuda(), 6)
+    torch.cuda.synchronize()
+    assert via_api.values == dict(zip(vm.moment_indices(6), engine.i128_to_ints(direct.i128[0].cpu().numpy())))
