@@ -258,7 +258,8 @@ def main():
     if cfg != 5:
         graphed = engine.GraphedMoments(vox, order, offset=offset)   # captured once, replayed per step
     else:
-        stages = engine.GraphedSlabStages(vox, order, offset=offset, z0=z0)   # three graphs; all-reduce between
+        # three graphs with the all-reduce between; one device: the epilogue rides the moments launch
+        stages = engine.GraphedSlabStages(vox, order, offset=offset, z0=z0, fused=(world == 1))
 
     def step(i=None):
         if cfg == 5:

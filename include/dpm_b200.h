@@ -156,6 +156,13 @@ DPM_API int dpm_project_profile(const dpm_volume_desc* desc, const void* d_voxel
  * entries of slot DPM_IMG_ZX): a DPM_ACC_PROFILE accumulator, zeroed first. */
 DPM_API int dpm_moments2d_profile(const dpm_volume_desc* desc, int order, const uint32_t* const* d_images,
                 const uint64_t* d_profile, uint64_t* d_acc, void* stream);
+/* The same, ending with the epilogue in the same launch (the last block of each
+ * volume derives it, like dpm_moments): for a single device, where no
+ * accumulator exchange sits between the moments and the epilogue.
+ * d_counters: B uint32 scratch (zeroed by the call). */
+DPM_API int dpm_moments2d_profile_derive(const dpm_volume_desc* desc, int order, const uint32_t* const* d_images,
+                const uint64_t* d_profile, uint64_t* d_acc, uint32_t* d_counters, int64_t* d_m3d_i128,
+                double* d_m3d_f64, int32_t* d_status, void* stream);
 /* Both steps on caller scratch of dpm_partial_workspace_bytes() bytes: the
  * per-slab partial of the multi-GPU / streaming drivers (accumulators of
  * z-slabs taken in global coordinates add elementwise). */

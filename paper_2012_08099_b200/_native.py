@@ -28,7 +28,7 @@ EXPORTS = (
     "dpm_workspace_bytes", "dpm_moments", "dpm_check_envelope", "dpm_acc_add",
     "dpm_synth_noise_u16", "dpm_last_launch_count", "dpm_strerror", "dpm_image_moments2d",
     "dpm_project_generic", "dpm_profile_layout", "dpm_project_profile", "dpm_moments2d_profile",
-    "dpm_partial_workspace_bytes", "dpm_moments_partial",
+    "dpm_partial_workspace_bytes", "dpm_moments_partial", "dpm_moments2d_profile_derive",
 )
 
 
@@ -72,6 +72,8 @@ def lib() -> ctypes.CDLL:
                                               ctypes.POINTER(ctypes.c_int)]),
         "dpm_project_profile": (ctypes.c_int, [pdesc, vp, ctypes.c_int, ctypes.POINTER(vp), vp, vp]),
         "dpm_moments2d_profile": (ctypes.c_int, [pdesc, ctypes.c_int, ctypes.POINTER(vp), vp, vp, vp]),
+        "dpm_moments2d_profile_derive": (ctypes.c_int, [pdesc, ctypes.c_int, ctypes.POINTER(vp), vp, vp, vp, vp, vp,
+                                                         vp, vp]),
         "dpm_partial_workspace_bytes": (sz, [pdesc, ctypes.c_int]),
         "dpm_moments_partial": (ctypes.c_int, [pdesc, vp, ctypes.c_int, vp, sz, vp, vp]),
         "dpm_image_moments2d": (ctypes.c_int, [vp, i64, i64, i64, i64, ctypes.c_int, vp, vp]),

@@ -243,6 +243,27 @@ int dpm_moments2d_profile(const dpm_volume_desc* desc, int order, const uint32_t
   return moments2d_profile_launch(desc, order, d_images, d_profile, d_acc, st);
 }
 
+int dpm_moments2d_profile_derive(const dpm_volume_desc* desc, int order, const uint32_t* const* d_images,
+                                 const uint64_t* d_profile, uint64_t* d_acc, uint32_t* d_counters,
+                                 int64_t* d_m3d_i128, double* d_m3d_f64, int32_t* d_status, void* stream) {
+  reset_launches();
+  int rc = check_desc(desc);
+  if (rc) return rc;
+  if (check_order(order) || !d_images || !d_profile || !d_acc || !d_counters || !d_m3d_i128 || !d_status)
+    return DPM_EINVAL;
+  const int n_img = num_images(order);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(d_acc, 0, (size_t)(desc->B * n_img * n2d(order) * 4) * sizeof(uint64_t), st) != cudaSuccess ||
+      cudaMemsetAsync(d_counters, 0, (size_t)desc->B * sizeof(uint32_t), st) != cudaSuccess)
+    return DPM_ECUDA;
+  FusedOut f;
+  f.cnt = d_counters;
+  f.i128 = d_m3d_i128;
+  f.f64 = d_m3d_f64;
+  f.status = d_status;
+  return moments2d_profile_launch(desc, order, d_images, d_profile, d_acc, st, &f);
+}
+
 size_t dpm_partial_workspace_bytes(const dpm_volume_desc* desc, int order) {
   if (check_desc(desc) || check_order(order)) return 0;
   const ProfGeom pg = profile_geom(desc, order);

@@ -371,9 +371,13 @@ class GraphedSlabStages:
     multi-GPU caller all-reduces ``acc`` between (2) and (3) (the exchange is
     not captured).  Replays are issued on the caller's current stream."""
 
-    def __init__(self, vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0):
+    def __init__(self, vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0, fused: bool = False):
+        """``fused``: single device, no exchange between (2) and (3): stage 2
+        ends with the epilogue in the same launch and ``replay_derive`` only
+        returns ``out``."""
         check_order(order)
         self.vox, self.order, self.offset, self.z0 = vox, order, offset, z0
+        self.fused = fused
         desc = make_desc(vox, offset, z0)
         n_img = num_images(order)
         dev = vox.device
@@ -388,7 +392,8 @@ class GraphedSlabStages:
             i128=torch.empty((desc.B, n3d(order), 2), dtype=torch.int64, device=dev),
             f64=torch.empty((desc.B, n3d(order)), dtype=torch.float64, device=dev),
             status=torch.empty((desc.B,), dtype=torch.int32, device=dev), launches=0)
-        stages = [self._project, self._moments2d, self._derive]
+        self.counters = torch.empty((desc.B,), dtype=torch.int32, device=dev)
+        stages = [self._project, self._moments2d] + ([] if fused else [self._derive])
         st = torch.cuda.Stream(device=dev)
         st.wait_stream(torch.cuda.current_stream(dev))
         self.graphs, self.launches = [], 0
@@ -407,7 +412,15 @@ class GraphedSlabStages:
         project_profile(self.vox, self.order, self.offset, self.z0, imgs=self.imgs, profile=self.profile)
 
     def _moments2d(self):
-        moments2d_profile(self.vox, self.imgs, self.profile, self.order, self.offset, self.z0, acc=self.acc)
+        if self.fused:
+            desc = make_desc(self.vox, self.offset, self.z0)
+            ptrs = (ctypes.c_void_p * len(self.imgs))(*[t.data_ptr() if t is not None else None for t in self.imgs])
+            nat.check(nat.lib().dpm_moments2d_profile_derive(
+                ctypes.byref(desc), self.order, ptrs, self.profile.data_ptr(), self.acc.data_ptr(),
+                self.counters.data_ptr(), self.out.i128.data_ptr(), self.out.f64.data_ptr(),
+                self.out.status.data_ptr(), stream_handle(None)), "dpm_moments2d_profile_derive")
+        else:
+            moments2d_profile(self.vox, self.imgs, self.profile, self.order, self.offset, self.z0, acc=self.acc)
 
     def _derive(self):
         derive(self.acc, self.order, out=self.out)
@@ -420,7 +433,8 @@ class GraphedSlabStages:
         return self.acc
 
     def replay_derive(self) -> DeviceMoments:
-        self.graphs[2].replay()
+        if not self.fused:
+            self.graphs[2].replay()
         return self.out
 
 

@@ -167,3 +167,19 @@ def test_public_api_upload_path_is_exact():
     direct = engine.moments(torch.from_numpy(vol).cuda(), 6)
     torch.cuda.synchronize()
     assert via_api.values == dict(zip(vm.moment_indices(6), engine.i128_to_ints(direct.i128[0].cpu().numpy())))
+
+
+@pytest.mark.parametrize("order", [4, 6])
+def test_graphed_slab_stages_fused_epilogue(order):
+    """Single-device stages: the epilogue riding the moments launch gives the
+    same exact moments as the separate derive stage."""
+    rng = np.random.default_rng(order + 3)
+    vol = torch.from_numpy(rng.integers(0, 65535, size=(120, 30, 264)).astype(np.uint16)).cuda()
+    sep = engine.GraphedSlabStages(vol, order, z0=5)
+    fused = engine.GraphedSlabStages(vol, order, z0=5, fused=True)
+    assert fused.launches == 2
+    for _ in range(2):
+        sep.replay_project(); sep.replay_moments2d(); a = sep.replay_derive()
+        fused.replay_project(); fused.replay_moments2d(); b = fused.replay_derive()
+        torch.cuda.synchronize()
+        assert torch.equal(a.i128, b.i128) and torch.equal(a.status, b.status) and int(b.status[0]) == 0
