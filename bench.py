@@ -394,7 +394,7 @@ def run_e2e(args, cfg, order, offset, vox, z0, n_global, world, rank, dev, total
         if not zslab and h2d <= (4 << 30):
             # fits on the device in one piece: H2D + pipeline + D2H captured in one CUDA graph
             hg = engine.HostGraphedMoments(host, order, offset=offset, device=dev)
-            path = "paper_2012_08099_b200.engine.HostGraphedMoments (pinned host, one graph: H2D, 3 kernels, D2H)"
+            path = "paper_2012_08099_b200.engine.HostGraphedMoments (pinned host, one graph: H2D, projection + moments/epilogue kernels, D2H)"
 
             def step():
                 return hg.run()
