@@ -405,7 +405,7 @@ def run_e2e(args, cfg, order, offset, vox, z0, n_global, world, rank, dev, total
             def step():
                 acc = streamer.run(host, offset=offset, z_base=z0, n_global=n_global)
                 pdist.allreduce_limbs(acc)
-                res = engine.derive(acc, order)
+                res = engine.derive(acc, order, kind=engine.acc_kind(vox, order))
                 return res.i128.to("cpu", non_blocking=False), res.status.to("cpu", non_blocking=False)
         torch.cuda.synchronize()
 

@@ -73,6 +73,7 @@ extern "C" {
 /* ---- limb-accumulator kinds (what slot DPM_IMG_ZX of d_acc holds) ---------- */
 #define DPM_ACC_IMAGES 0   /* the ZX image's 2D moments (dpm_moments2d on dpm_project's images) */
 #define DPM_ACC_PROFILE 1  /* the y-summed profile's 1D moments (dpm_moments_partial, dpm_moments2d_profile) */
+#define DPM_ACC_PROFILE_T 2 /* the same for layout T (x and z exchanged, see dpm_moments_acc_kind) */
 
 /* A (batch of) volume(s), or a z-slab of one.  Strides are in elements. */
 typedef struct dpm_volume_desc {
@@ -144,9 +145,26 @@ DPM_API int dpm_image_moments2d(const uint32_t* d_pixels, int64_t W, int64_t H, 
  * a 1D array of WQ = L + |t|(N-1) uint64 per volume (stored index x + t z, plus
  * |t|(N-1) when t < 0; logical coordinate = stored index + ai).  Per voxel the
  * pass folds the profile into a register window summed over y instead of
- * keeping the 8 x VX ZX accumulators of dpm_project.  The images it does build
- * are bit-identical to dpm_project's. */
+ * keeping the 8 x VX ZX accumulators of dpm_project.
+ *
+ * Layout T.  Wide volumes (L >= 192) build that image set for the volume with
+ * x and z EXCHANGED, V'(x', y, z') = V(z', y, x'), with the z-streaming kernel:
+ * XY slot (z, y) stored [y][z]; YZ slot (y, x) stored [x][y]; DIAG z + x,
+ * ANTI z - x + (L-1), X2P z + 2x, X2M z - 2x + 2(L-1) stored [y][.]; the
+ * profile P[z + t x] (+|t|(L-1) when t < 0), WQ = N + |t|(L-1).  Their
+ * accumulators are DPM_ACC_PROFILE_T (the epilogue relabels M_pqr = M'_rqp).
+ * The layout depends on the geometry only, so all z-slabs of one volume agree.
+ * dpm_moments_image_layout / dpm_profile_layout give the geometry of the
+ * moments pipeline's images and profile for either layout. */
 DPM_API int dpm_profile_layout(const dpm_volume_desc* desc, int order, int64_t* WQ, int64_t* ai, int* t);
+/* Accumulator kind (DPM_ACC_PROFILE or DPM_ACC_PROFILE_T) that
+ * dpm_moments_partial / dpm_moments2d_profile produce for `desc`, to pass to
+ * dpm_derive3d; negative on a bad argument. */
+DPM_API int dpm_moments_acc_kind(const dpm_volume_desc* desc, int order);
+/* Geometry of image `img` (not DPM_IMG_ZX) of the moments pipeline at `order`
+ * (as dpm_image_layout, for the layout dpm_moments_acc_kind names). */
+DPM_API int dpm_moments_image_layout(const dpm_volume_desc* desc, int order, int img,
+                int64_t* W, int64_t* H, int64_t* ai, int64_t* aj);
 /* Projection pass of the moments pipeline: images 0..num_images(order)-1
  * except DPM_IMG_ZX (d_images[2] is ignored) plus the profile (B * WQ
  * uint64).  Zeroes its outputs first. */

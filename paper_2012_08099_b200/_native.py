@@ -13,13 +13,14 @@ import os
 from functools import lru_cache
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdpm_b200.so")
+# DPM_LIB_PATH overrides the in-tree library (A/B builds of kernel variants only)
+LIB_PATH = os.environ.get("DPM_LIB_PATH") or os.path.join(_HERE, "libdpm_b200.so")
 
 DPM_OK, DPM_EINVAL, DPM_EOVERFLOW, DPM_ECUDA, DPM_EWORKSPACE = 0, 1, 2, 3, 4
 DPM_ST_DISAGREE, DPM_ST_NONEXACT, DPM_ST_MASS = 1, 2, 4
 DPM_U8, DPM_U16, DPM_I16 = 1, 2, 3
 MAX_IMAGES, MAX_ORDER = 7, 6
-DPM_ACC_IMAGES, DPM_ACC_PROFILE = 0, 1
+DPM_ACC_IMAGES, DPM_ACC_PROFILE, DPM_ACC_PROFILE_T = 0, 1, 2
 
 #: every symbol include/dpm_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = (
@@ -29,6 +30,7 @@ EXPORTS = (
     "dpm_synth_noise_u16", "dpm_last_launch_count", "dpm_strerror", "dpm_image_moments2d",
     "dpm_project_generic", "dpm_profile_layout", "dpm_project_profile", "dpm_moments2d_profile",
     "dpm_partial_workspace_bytes", "dpm_moments_partial", "dpm_moments2d_profile_derive",
+    "dpm_moments_acc_kind", "dpm_moments_image_layout",
 )
 
 
@@ -63,6 +65,8 @@ def lib() -> ctypes.CDLL:
         "dpm_num_moments3d": (ctypes.c_int, [ctypes.c_int]),
         "dpm_num_moments2d": (ctypes.c_int, [ctypes.c_int]),
         "dpm_image_layout": (ctypes.c_int, [pdesc, ctypes.c_int] + [ctypes.POINTER(i64)] * 4),
+        "dpm_moments_image_layout": (ctypes.c_int, [pdesc, ctypes.c_int, ctypes.c_int] + [ctypes.POINTER(i64)] * 4),
+        "dpm_moments_acc_kind": (ctypes.c_int, [pdesc, ctypes.c_int]),
         "dpm_project_workspace_bytes": (sz, [pdesc, ctypes.c_int]),
         "dpm_project": (ctypes.c_int, [pdesc, vp, ctypes.c_int, ctypes.POINTER(vp), vp, sz, vp]),
         "dpm_project_generic": (ctypes.c_int, [pdesc, vp, ctypes.c_int, ctypes.POINTER(vp), vp]),

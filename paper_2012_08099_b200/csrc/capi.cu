@@ -1,16 +1,26 @@
 // capi.cu -- the C ABI (include/dpm_b200.h): argument validation, workspace
 // carving and stage dispatch.  No allocation, no synchronisation.
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include "dpm_common.cuh"
 
 namespace dpm {
 
 static thread_local int g_launches = 0;
+// DPM_DEBUG=1 in the environment: CUDA errors behind DPM_ECUDA are printed
+void report_cuda_error(cudaError_t e, const char* where) {
+  static const bool on = getenv("DPM_DEBUG") != nullptr;
+  if (on) fprintf(stderr, "[dpm] CUDA error in %s: %s\n", where, cudaGetErrorString(e));
+}
 void note_launches(int n) { g_launches += n; }
 void reset_launches() { g_launches = 0; }
 
 int launch_project_generic(const dpm_volume_desc* d, const void* vox, const ImageSet& s, unsigned long long* prof,
-                           cudaStream_t st);
+                           cudaStream_t st, bool transposed = false);
+int launch_project_zstream(const dpm_volume_desc* d, const void* vox, int order, const ImageSet& s,
+                           unsigned long long* prof, int64_t WQ, cudaStream_t st, bool* handled);
+bool zstream_eligible(const dpm_volume_desc* d, const void* vox);
 int launch_project_stream(const dpm_volume_desc* d, const void* vox, const ImageSet& s, unsigned long long* prof,
                           cudaStream_t st, bool* handled);
 int profile_shift(int n_img);
@@ -44,14 +54,39 @@ static int check_desc(const dpm_volume_desc* d) {
 
 static int check_order(int order) { return (order >= 3 && order <= DPM_MAX_ORDER) ? DPM_OK : DPM_EINVAL; }
 
-// no_zx: moments-pipeline image set (slot 2 empty: W = H = 0, no pointer)
+// Moments-pipeline layout.  Wide volumes use layout T: the
+// method's image set of the volume with x and z exchanged, built by the
+// z-streaming kernel (project_zstream.cu); the epilogue relabels the result.
+// A pure function of the geometry (never of pointers), so the z-slabs of one
+// volume -- whose accumulators are summed across ranks -- always agree.
+// (DPM_LAYOUT_T_MIN_L in the environment moves the threshold: A/B timing only)
+static int64_t layout_t_min_l() {
+  static const int64_t v = [] {
+    const char* e = getenv("DPM_LAYOUT_T_MIN_L");
+    return e ? (int64_t)atoll(e) : (int64_t)192;
+  }();
+  return v;
+}
+static bool layout_t(const dpm_volume_desc* d) { return d->L >= layout_t_min_l(); }
+
+// stored geometry of image k of the moments pipeline (slot ZX unused)
+static ImageGeom mgeom(const dpm_volume_desc* d, int k) {
+  if (!layout_t(d)) return image_geom(d->L, d->M, d->N, d->z0, k);
+  // transposed volume V'(x', y, z') = V(z', y, x'): L' = N, N' = L; the slab's
+  // global z offset shifts x', i.e. every image index that contains x'
+  ImageGeom g = image_geom(d->N, d->M, d->L, 0, k);
+  if (k == DPM_IMG_XY || k >= DPM_IMG_DIAG) g.ai += d->z0;
+  return g;
+}
+
+// no_zx: moments-pipeline image set (slot 2 empty: W = H = 0, no pointer; layout per mgeom)
 static ImageSet make_set(const dpm_volume_desc* d, int n_img, uint32_t* const* imgs, bool no_zx = false) {
   ImageSet s;
   memset(&s, 0, sizeof(s));
   s.n_img = n_img;
   for (int k = 0; k < n_img; ++k) {
     if (no_zx && k == DPM_IMG_ZX) continue;
-    const ImageGeom g = image_geom(d->L, d->M, d->N, d->z0, k);
+    const ImageGeom g = no_zx ? mgeom(d, k) : image_geom(d->L, d->M, d->N, d->z0, k);
     s.img[k] = imgs ? imgs[k] : nullptr;
     s.W[k] = g.W; s.H[k] = g.H; s.ai[k] = g.ai; s.aj[k] = g.aj;
   }
@@ -63,7 +98,7 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 static size_t images_bytes(const dpm_volume_desc* d, int n_img, size_t* offs, bool no_zx = false) {
   size_t total = 0;
   for (int k = 0; k < n_img; ++k) {
-    const ImageGeom g = image_geom(d->L, d->M, d->N, d->z0, k);
+    const ImageGeom g = no_zx ? mgeom(d, k) : image_geom(d->L, d->M, d->N, d->z0, k);
     if (offs) offs[k] = total;
     if (no_zx && k == DPM_IMG_ZX) continue;
     total += align256((size_t)(g.W * g.H * d->B) * sizeof(uint32_t));
@@ -82,15 +117,23 @@ static ProfGeom profile_geom(const dpm_volume_desc* d, int order) {
   ProfGeom g;
   g.t = profile_shift(num_images(order));
   const int64_t at = g.t < 0 ? -g.t : g.t;
-  g.WQ = d->L + at * (d->N - 1);
-  g.ai = g.t > 0 ? g.t * d->z0 : -at * (d->N - 1) - at * d->z0;
+  if (layout_t(d)) {   // P[z + t x] (+|t|(L-1) for t < 0); the slab offset shifts z
+    g.WQ = d->N + at * (d->L - 1);
+    g.ai = (g.t > 0 ? 0 : -at * (d->L - 1)) + d->z0;
+  } else {
+    g.WQ = d->L + at * (d->N - 1);
+    g.ai = g.t > 0 ? g.t * d->z0 : -at * (d->N - 1) - at * d->z0;
+  }
   return g;
 }
 
-static int jbits_for(const dpm_volume_desc* d, int n_img) {
+static int acc_kind_of(const dpm_volume_desc* d) { return layout_t(d) ? DPM_ACC_PROFILE_T : DPM_ACC_PROFILE; }
+
+static int jbits_for(const dpm_volume_desc* d, int n_img, bool moments_set = false) {
   int64_t jmax = 0;
   for (int k = 0; k < n_img; ++k) {
-    const ImageGeom g = image_geom(d->L, d->M, d->N, d->z0, k);
+    if (moments_set && k == DPM_IMG_ZX) continue;
+    const ImageGeom g = moments_set ? mgeom(d, k) : image_geom(d->L, d->M, d->N, d->z0, k);
     jmax = imax64(jmax, g.H - 1 + g.aj);
   }
   int b = 0;
@@ -177,6 +220,13 @@ static int project_profile_launch(const dpm_volume_desc* desc, const void* d_vox
   ImageSet s = make_set(desc, num_images(order), d_images, true);
   unsigned long long* prof = reinterpret_cast<unsigned long long*>(d_profile);
   bool handled = false;
+  if (layout_t(desc)) {
+    const int rc = launch_project_zstream(desc, d_voxels, order, s, prof, profile_geom(desc, order).WQ, st, &handled);
+    if (rc || handled) return rc;
+    // shapes the z-streaming kernel cannot read (unaligned rows): the generic
+    // brick kernel on the transposed view builds the same layout-T images
+    return launch_project_generic(desc, d_voxels, s, prof, st, true);
+  }
   const int rc = launch_project_stream(desc, d_voxels, s, prof, st, &handled);
   if (rc || handled) return rc;
   if (!images_zeroed)
@@ -196,10 +246,11 @@ static int moments2d_profile_launch(const dpm_volume_desc* desc, int order, cons
                                     const FusedOut* fused = nullptr) {
   const int n_img = num_images(order);
   ImageSet s = make_set(desc, n_img, const_cast<uint32_t* const*>(d_images), true);
-  const int jb = jbits_for(desc, n_img);
+  const int jb = jbits_for(desc, n_img, true);
   if (jb > 21) return DPM_EOVERFLOW;
   const ProfGeom pg = profile_geom(desc, order);
   M2Extra ex;
+  ex.kind = acc_kind_of(desc);
   ex.prof = reinterpret_cast<const unsigned long long*>(d_profile);
   ex.WQ = pg.WQ;
   ex.ai = pg.ai;
@@ -292,7 +343,7 @@ static int moments_partial_impl(const dpm_volume_desc* desc, const void* d_voxel
   // one zeroing of the contiguous images + profile scratch, one of the accumulator
   // (or none when the caller's accumulator directly precedes it: dpm_moments)
   // (single-tile volumes: the images are stored whole by the kernel, zero only the profile and counters)
-  const bool single = project_stream_single_tile(desc, d_voxels, n_img);
+  const bool single = !layout_t(desc) && project_stream_single_tile(desc, d_voxels, n_img);
   const size_t tail = dpm_partial_workspace_bytes(desc, order) - ib +
                       (fused ? align256((size_t)desc->B * sizeof(unsigned int)) : 0);
   char* z0 = single ? reinterpret_cast<char*>(prof) : base;
@@ -347,7 +398,7 @@ int dpm_derive3d(const dpm_volume_desc* desc, const uint64_t* d_acc, int order, 
                  double* d_m3d_f64, int32_t* d_status, void* stream) {
   reset_launches();
   if (!desc || desc->B < 1 || check_order(order) || !d_acc || !d_m3d_i128 || !d_status) return DPM_EINVAL;
-  if (acc_kind != DPM_ACC_IMAGES && acc_kind != DPM_ACC_PROFILE) return DPM_EINVAL;
+  if (acc_kind != DPM_ACC_IMAGES && acc_kind != DPM_ACC_PROFILE && acc_kind != DPM_ACC_PROFILE_T) return DPM_EINVAL;
   return launch_derive3d(d_acc, desc->B, num_images(order), order, acc_kind, d_m3d_i128, d_m3d_f64, d_status,
                          static_cast<cudaStream_t>(stream));
 }
@@ -433,7 +484,7 @@ static int moments_staged(const dpm_volume_desc* desc, const Staged& g, const vo
     launches += dpm_last_launch_count();
     if (rc) return rc;
   }
-  const int rc = dpm_derive3d(desc, acc, order, DPM_ACC_PROFILE, d_m3d_i128, d_m3d_f64, d_status, stream);
+  const int rc = dpm_derive3d(desc, acc, order, acc_kind_of(&g.slab), d_m3d_i128, d_m3d_f64, d_status, stream);
   g_launches = launches + dpm_last_launch_count();
   return rc;
 }
@@ -442,7 +493,8 @@ int dpm_check_envelope(int64_t L, int64_t M, int64_t N_global, int64_t vmax, int
   if (L < 1 || M < 1 || N_global < 1 || vmax < 0 || check_order(order)) return DPM_EINVAL;
   // every |moment| and every partial sum <= mass * cmax^K, cmax = largest |logical coordinate|
   const long double mass = (long double)vmax * L * M * N_global;
-  const int64_t cmax = imax64(imax64(L, M), L + 2 * N_global);
+  // (x +- 2z images of the classic layout, z +- 2x of layout T)
+  const int64_t cmax = imax64(imax64(L, M), imax64(L + 2 * N_global, N_global + 2 * L));
   long double bound = mass;
   for (int k = 0; k < order; ++k) bound *= (long double)cmax;
   if (bound >= 0x1p126L) return DPM_EOVERFLOW;
@@ -486,6 +538,23 @@ int dpm_synth_noise_u16(uint16_t* d_out, int64_t L, int64_t M, int64_t z0, int64
   reset_launches();
   if (!d_out || L < 1 || M < 1 || z0 < 0 || n_planes < 1) return DPM_EINVAL;
   return launch_synth_noise(d_out, L, M, z0, n_planes, seed, static_cast<cudaStream_t>(stream));
+}
+
+int dpm_moments_acc_kind(const dpm_volume_desc* desc, int order) {
+  if (check_desc(desc) || check_order(order)) return -DPM_EINVAL;
+  return acc_kind_of(desc);
+}
+
+int dpm_moments_image_layout(const dpm_volume_desc* desc, int order, int img, int64_t* W, int64_t* H, int64_t* ai,
+                             int64_t* aj) {
+  if (check_desc(desc) || check_order(order) || img < 0 || img >= num_images(order) || img == DPM_IMG_ZX)
+    return DPM_EINVAL;
+  const ImageGeom g = mgeom(desc, img);
+  if (W) *W = g.W;
+  if (H) *H = g.H;
+  if (ai) *ai = g.ai;
+  if (aj) *aj = g.aj;
+  return DPM_OK;
 }
 
 int dpm_last_launch_count(void) { return g_launches; }

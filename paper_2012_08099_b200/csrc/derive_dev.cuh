@@ -77,7 +77,10 @@ __device__ __forceinline__ int64_t binom(int n, int k) {
 template <int K>
 __device__ void derive_volume(const uint64_t* a, int64_t b, int n_img, int kind, int64_t* out_i128, double* out_f64,
                               int32_t* status, uint64_t* sa, int32_t* sst_p, bool coherent) {
-  const bool prof = kind == DPM_ACC_PROFILE;
+  // DPM_ACC_PROFILE_T: the accumulator holds the layout-T image set (the volume
+  // with x and z exchanged); the solve yields M'_pqr = M_rqp, stored relabelled
+  const bool prof = kind == DPM_ACC_PROFILE || kind == DPM_ACC_PROFILE_T;
+  const bool tr = kind == DPM_ACC_PROFILE_T;
   constexpr int N2 = (K + 1) * (K + 2) / 2;
   constexpr int N3 = (K + 1) * (K + 2) * (K + 3) / 6;
   int32_t& sst = *sst_p;
@@ -88,7 +91,8 @@ __device__ void derive_volume(const uint64_t* a, int64_t b, int n_img, int kind,
   __syncthreads();
   int32_t st = 0;
   auto m2 = [&](int img, int p, int q) -> i128 { return acc_to_i128(sa + (img * N2 + idx2(K, p, q)) * 4); };
-  auto put = [&](int i, i128 v) {
+  auto put = [&](int p, int q, int r, i128 v) {
+    const int i = tr ? idx3(K, r, q, p) : idx3(K, p, q, r);
     const unsigned __int128 u = (unsigned __int128)v;
     out_i128[(b * N3 + i) * 2 + 0] = (int64_t)(uint64_t)u;
     out_i128[(b * N3 + i) * 2 + 1] = (int64_t)(uint64_t)(u >> 64);
@@ -112,7 +116,7 @@ __device__ void derive_volume(const uint64_t* a, int64_t b, int n_img, int kind,
           if (r == 0) route(m2(DPM_IMG_XY, p, q));
           if (p == 0) route(m2(DPM_IMG_YZ, q, r));
           if (q == 0 && !prof) route(m2(DPM_IMG_ZX, r, p));
-          put(n, v);
+          put(p, q, r, v);
         }
   }
 
@@ -184,7 +188,7 @@ __device__ void derive_volume(const uint64_t* a, int64_t b, int n_img, int kind,
           if (c <= n) {
             i128 m = 0;
             ok &= div_exact(u[c], binom(p, c), &m);
-            put(idx3(K, p - c, q, c), m);
+            put(p - c, q, c, m);
           }
         }
         if (!ok) st |= DPM_ST_NONEXACT;

@@ -1,5 +1,6 @@
 // dpm_common.cuh -- shared geometry and launch plumbing for the DPM kernels.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "../../include/dpm_b200.h"
@@ -64,6 +65,7 @@ template <> struct VoxelTraits<int16_t>  { static __device__ __forceinline__ uin
 struct M2Extra {
   const unsigned long long* prof;
   int64_t WQ, ai;
+  int kind;                 // accumulator kind of the fused epilogue (DPM_ACC_PROFILE / _T)
   unsigned int* cnt;
   int64_t* out_i128;
   double* out_f64;
@@ -76,13 +78,38 @@ void reset_launches();
 
 }  // namespace dpm
 
+namespace dpm { void report_cuda_error(cudaError_t e, const char* where); }
 #define DPM_CUDA_CHECK_LAUNCH()                                  \
   do {                                                           \
     cudaError_t _e = cudaGetLastError();                         \
-    if (_e != cudaSuccess) return DPM_ECUDA;                     \
+    if (_e != cudaSuccess) {                                     \
+      dpm::report_cuda_error(_e, __FILE__);                      \
+      return DPM_ECUDA;                                          \
+    }                                                            \
   } while (0)
 
 namespace dpm {
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
+}  // namespace dpm
+
+namespace dpm {
+// Dynamic shared-memory opt-in of one kernel, set once per DEVICE (the
+// attribute lives in that device's context; a process-wide once-flag would
+// leave a second GPU unconfigured).  `mask` is the kernel's own bit set of
+// configured device ordinals.
+template <typename KernelT>
+inline int ensure_smem(KernelT kern, size_t bytes, std::atomic<uint64_t>& mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return DPM_ECUDA;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return DPM_OK;
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) {
+    report_cuda_error(e, "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
+    return DPM_ECUDA;
+  }
+  mask.fetch_or(bit, std::memory_order_acq_rel);
+  return DPM_OK;
+}
 }  // namespace dpm

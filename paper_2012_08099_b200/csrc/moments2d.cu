@@ -50,6 +50,7 @@ struct M2Params {
   int64_t* out_i128;
   double* out_f64;
   int32_t* status;
+  int kind;
 };
 
 // one block's share of the profile's 1D moments (cells chunk, chunk + pblocks, ...)
@@ -217,31 +218,30 @@ __global__ void __launch_bounds__(M2_THREADS) moments2d_kernel(M2Params p) {
     __syncthreads();
     if (last) {
       __threadfence();
-      derive_volume<K>(p.acc + b * p.s.n_img * N2 * 4, b, p.s.n_img, DPM_ACC_PROFILE, p.out_i128, p.out_f64,
+      derive_volume<K>(p.acc + b * p.s.n_img * N2 * 4, b, p.s.n_img, p.kind, p.out_i128, p.out_f64,
                        p.status, reinterpret_cast<uint64_t*>(m2_smem), &sst, true);
     }
   }
 }
 
 template <int K, int JB>
-static void launch_kj(dim3 grid, cudaStream_t st, const M2Params& p) {
+static int launch_kj(dim3 grid, cudaStream_t st, const M2Params& p) {
   constexpr int NT = Limbs<JB>::off(K + 1);
   constexpr int NTP = (NT + 3) & ~3;
   constexpr int N2 = (K + 1) * (K + 2) / 2;
   constexpr size_t t_bytes = 256 * NTP * 4, r_bytes = (size_t)M2_CHUNK * 4 * (M2_THREADS + 1) * 4;
   constexpr size_t bytes = t_bytes > r_bytes ? t_bytes : r_bytes;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(moments2d_kernel<K, JB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  });
+  static std::atomic<uint64_t> attr_mask{0};
+  if (ensure_smem(moments2d_kernel<K, JB>, bytes, attr_mask)) return DPM_ECUDA;
   moments2d_kernel<K, JB><<<grid, M2_THREADS, bytes, st>>>(p);
+  return DPM_OK;
 }
 
 template <int K>
-static void launch_k(int jb, dim3 grid, cudaStream_t st, const M2Params& p) {
-  if (jb <= 12) launch_kj<K, 12>(grid, st, p);
-  else if (jb <= 16) launch_kj<K, 16>(grid, st, p);
-  else launch_kj<K, 21>(grid, st, p);
+static int launch_k(int jb, dim3 grid, cudaStream_t st, const M2Params& p) {
+  if (jb <= 12) return launch_kj<K, 12>(grid, st, p);
+  if (jb <= 16) return launch_kj<K, 16>(grid, st, p);
+  return launch_kj<K, 21>(grid, st, p);
 }
 
 int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_t* acc, cudaStream_t st,
@@ -256,6 +256,7 @@ int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_
   p.out_i128 = ex ? ex->out_i128 : nullptr;
   p.out_f64 = ex ? ex->out_f64 : nullptr;
   p.status = ex ? ex->status : nullptr;
+  p.kind = ex ? ex->kind : DPM_ACC_PROFILE;
   // rows per chunk: the largest of 256/128/64 that still gives >= 8 CTAs per SM
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -280,12 +281,14 @@ int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_
   if (nblocks == 0) return DPM_OK;
   if (nblocks > 0x7fffffffLL) return DPM_EINVAL;
   dim3 grid((unsigned)nblocks);
+  int rc;
   switch (order) {
-    case 3: launch_k<3>(jbits, grid, st, p); break;
-    case 4: launch_k<4>(jbits, grid, st, p); break;
-    case 5: launch_k<5>(jbits, grid, st, p); break;
-    default: launch_k<6>(jbits, grid, st, p); break;
+    case 3: rc = launch_k<3>(jbits, grid, st, p); break;
+    case 4: rc = launch_k<4>(jbits, grid, st, p); break;
+    case 5: rc = launch_k<5>(jbits, grid, st, p); break;
+    default: rc = launch_k<6>(jbits, grid, st, p); break;
   }
+  if (rc) return rc;
   note_launches(1);
   DPM_CUDA_CHECK_LAUNCH();
   return DPM_OK;

@@ -18,7 +18,7 @@ constexpr int GWQ = GBX + 3 * (GBZ - 1);  // profile footprint width (|t| <= 3)
 struct GenericParams {
   const void* vox;
   int64_t L, M, N, B;
-  int64_t sy, sz, sb;
+  int64_t sx, sy, sz, sb;   // element strides (sx = 1 except for the transposed view)
   int32_t offset;
   int64_t nbx, nby, nbz;
   ImageSet s;
@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(256) project_generic_kernel(GenericParams p) {
 
     const int64_t x = x0 + xl, y = y0 + yl;
     const bool valid = (x < p.L) && (y < p.M);
-    const T* row = vox + b * p.sb + y * p.sy + x;
+    const T* row = vox + b * p.sb + y * p.sy + x * p.sx;
     uint32_t xy = 0;
     const int zcount = (int)imin64(GBZ, p.N - z0);
     for (int zl = 0; zl < zcount; ++zl) {
@@ -135,20 +135,25 @@ __global__ void __launch_bounds__(256) project_generic_kernel(GenericParams p) {
 
 int profile_shift(int n_img);
 
-// prof != nullptr: moments mode (the profile along x + t z replaces ZX)
+// prof != nullptr: moments mode (the profile along x + t z replaces ZX).
+// transposed: the volume is read as V'(x', y, z') = V(z', y, x') -- the
+// moments pipeline's layout T (capi.cu) for shapes the z-streaming kernel
+// cannot read; `s` then carries the layout-T geometry
 int launch_project_generic(const dpm_volume_desc* d, const void* vox, const ImageSet& s, unsigned long long* prof,
-                           cudaStream_t st) {
+                           cudaStream_t st, bool transposed) {
   GenericParams p;
+  p.vox = vox; p.M = d->M; p.B = d->B;
+  p.sy = d->stride_y; p.sb = d->stride_b; p.offset = d->offset;
+  if (transposed) { p.L = d->N; p.N = d->L; p.sx = d->stride_z; p.sz = 1; }
+  else { p.L = d->L; p.N = d->N; p.sx = 1; p.sz = d->stride_z; }
   p.prof = prof;
   p.tq = profile_shift(s.n_img);
   {
     const int at = p.tq < 0 ? -p.tq : p.tq;
-    p.WQ = d->L + at * (d->N - 1);
-    p.qoff = p.tq < 0 ? at * (d->N - 1) : 0;
+    p.WQ = p.L + at * (p.N - 1);
+    p.qoff = p.tq < 0 ? at * (p.N - 1) : 0;
   }
-  p.vox = vox; p.L = d->L; p.M = d->M; p.N = d->N; p.B = d->B;
-  p.sy = d->stride_y; p.sz = d->stride_z; p.sb = d->stride_b; p.offset = d->offset;
-  p.nbx = (d->L + GBX - 1) / GBX; p.nby = (d->M + GBY - 1) / GBY; p.nbz = (d->N + GBZ - 1) / GBZ;
+  p.nbx = (p.L + GBX - 1) / GBX; p.nby = (p.M + GBY - 1) / GBY; p.nbz = (p.N + GBZ - 1) / GBZ;
   p.s = s;
   const int64_t total = p.nbx * p.nby * p.nbz * p.B;
   int dev = 0, sms = 148;

@@ -733,7 +733,7 @@ project_stream_kernel(const __grid_constant__ CUtensorMap tmap, const StreamPara
 // ---------------------------------------------------------------------------
 // host side
 
-static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -757,7 +757,7 @@ static bool stream_eligible(const dpm_volume_desc* d, const void* vox) {
   if (reinterpret_cast<uintptr_t>(vox) % 16) return false;
   if (d->L > 0x7fffffffLL || d->M > 0x7fffffffLL || d->N > 0x7fffffffLL || d->B > 0x7fffffffLL) return false;
   if (d->B * d->M > 0x7fffffffLL || d->L + 2 * d->N > 0x7fffffffLL) return false;   // 32-bit row ids / widths
-  return encode_fn() != nullptr;
+  return tensor_map_encoder() != nullptr;
 }
 
 size_t project_stream_workspace(const dpm_volume_desc*, int) { return 0; }
@@ -814,7 +814,7 @@ static int launch_one(const dpm_volume_desc* d, const void* vox, int grid, cudaS
                                  (cuuint64_t)((d->B > 1 ? d->stride_b : d->stride_z * d->N) * es)};
   const cuuint32_t box[4] = {(cuuint32_t)G::SX, 1, (cuuint32_t)G::SZ, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
-  const CUresult r = encode_fn()(&map, sizeof(T) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16,
+  const CUresult r = tensor_map_encoder()(&map, sizeof(T) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16,
                                  4, const_cast<void*>(vox), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -827,11 +827,8 @@ static int launch_one(const dpm_volume_desc* d, const void* vox, int grid, cudaS
   p.ntz = (d->N + G::SZ - 1) / G::SZ;
   p.ncol = p.ntx * p.ntz * d->B;
   p.single = (DPM_SINGLE_TILE && PROF && p.ntx == 1 && p.ntz == 1) ? 1u : 0u;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(project_stream_kernel<T, NI, NW, VX, S, PROF, ZP, CTAS>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  });
+  static std::atomic<uint64_t> attr_mask{0};
+  if (ensure_smem(project_stream_kernel<T, NI, NW, VX, S, PROF, ZP, CTAS>, bytes, attr_mask)) return DPM_ECUDA;
   project_stream_kernel<T, NI, NW, VX, S, PROF, ZP, CTAS>
       <<<(int)imin64((int64_t)grid * CTAS, p.ncol * d->M), 32 * NW, bytes, st>>>(map, p);
   return DPM_OK;

@@ -241,3 +241,27 @@ __device__ __forceinline__ void st_global_if(uint32_t* gptr, uint32_t v, bool pr
 }
 }  // namespace ptx
 }  // namespace dpm
+
+namespace dpm {
+namespace ptx {
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+template <typename V> __device__ __forceinline__ V lds_vec(uint32_t addr);
+template <> __device__ __forceinline__ uint4 lds_vec<uint4>(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr) : "memory");
+  return v;
+}
+template <> __device__ __forceinline__ uint2 lds_vec<uint2>(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+}  // namespace ptx
+}  // namespace dpm

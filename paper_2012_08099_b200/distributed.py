@@ -58,7 +58,7 @@ def moments_zslab(slab: torch.Tensor, order: int, z0: int, n_global: int, offset
     engine.check_envelope(d.L, d.M, n_global, d.dtype, order)
     acc = engine.moments2d_partial(slab, order, offset=offset, z0=z0, stream=stream)
     allreduce_limbs(acc, group)
-    return engine.derive(acc, order, stream=stream)
+    return engine.derive(acc, order, stream=stream, kind=engine.acc_kind(slab, order, offset, z0))
 
 
 def moments_batch_sharded(volumes: torch.Tensor, order: int, offset: int = 0, gather: bool = False, group=None):

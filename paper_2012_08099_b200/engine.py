@@ -44,10 +44,33 @@ def stream_handle(stream: torch.cuda.Stream | None = None) -> int:
     return int(s.cuda_stream)
 
 
-def make_desc(vox: torch.Tensor, offset: int = 0, z0: int = 0) -> nat.VolumeDesc:
-    """C-ABI descriptor of a [N,M,L] or [B,N,M,L] voxel tensor (x-contiguous)."""
+def check_voxel_range(vox: torch.Tensor, offset: int) -> None:
+    """int16 voxels are accumulated as ``v + offset`` in uint32 ray sums, which
+    is exact only when every ``v + offset`` lies in 0..65535 (the reference's
+    uint16 range, volume.py:34-35): check the actual data range (one device
+    reduction).  Unsigned voxels take no offset."""
+    if vox.dtype != torch.int16:
+        if offset != 0:
+            raise ValueError(f"offset {offset} given for {vox.dtype} voxels: offsets apply to int16 input only")
+        return
+    if not -32768 <= int(offset) <= 98303:
+        raise ValueError(f"offset {offset} cannot map int16 voxels into 0..65535")
+    if vox.numel() == 0 or (vox.is_cuda and torch.cuda.is_current_stream_capturing()):
+        return   # checked by the un-captured warm-up call (GraphedMoments & co.)
+    lo, hi = torch.aminmax(vox)
+    lo, hi = int(lo) + int(offset), int(hi) + int(offset)
+    if lo < 0 or hi > 65535:
+        raise ValueError(f"int16 voxels + offset {offset} span {lo}..{hi}, outside 0..65535 "
+                         f"(the exact uint32 accumulation needs unsigned 16-bit values)")
+
+
+def make_desc(vox: torch.Tensor, offset: int = 0, z0: int = 0, validate: bool = True) -> nat.VolumeDesc:
+    """C-ABI descriptor of a [N,M,L] or [B,N,M,L] voxel tensor (x-contiguous).
+    ``validate``: check the int16 + offset range (``check_voxel_range``)."""
     if vox.dtype not in _TORCH_DTYPE:
         raise ValueError(f"unsupported voxel dtype {vox.dtype}; use uint8, uint16 or int16(+offset)")
+    if validate:
+        check_voxel_range(vox, offset)
     if vox.dim() == 3:
         n, m, l = vox.shape
         b, sb = 1, vox.numel()
@@ -107,6 +130,27 @@ def image_layout(desc: nat.VolumeDesc, img: int) -> tuple[int, int, int, int]:
     nat.check(nat.lib().dpm_image_layout(ctypes.byref(desc), img, *[ctypes.byref(o) for o in out]),
               "dpm_image_layout")
     return tuple(int(o.value) for o in out)
+
+
+def moments_image_layout(desc: nat.VolumeDesc, order: int, img: int) -> tuple[int, int, int, int]:
+    """(W, H, ai, aj) of image ``img`` of the MOMENTS pipeline (its layout may
+    be layout T, the volume with x and z exchanged: see ``acc_kind``)."""
+    out = [ctypes.c_int64() for _ in range(4)]
+    nat.check(nat.lib().dpm_moments_image_layout(ctypes.byref(desc), order, img, *[ctypes.byref(o) for o in out]),
+              "dpm_moments_image_layout")
+    return tuple(int(o.value) for o in out)
+
+
+def acc_kind(vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0) -> str:
+    """Kind of the limb accumulator ``moments2d_partial`` / ``moments2d_profile``
+    produce for this volume: "profile" or "profile_t" (layout T, wide volumes);
+    pass it to ``derive``.  Depends on the geometry only, so every z-slab of a
+    volume gives the same kind."""
+    desc = make_desc(vox, offset, z0, validate=False)
+    k = int(nat.lib().dpm_moments_acc_kind(ctypes.byref(desc), order))
+    if k < 0:
+        nat.check(-k, "dpm_moments_acc_kind")
+    return {nat.DPM_ACC_PROFILE: "profile", nat.DPM_ACC_PROFILE_T: "profile_t"}[k]
 
 
 def project(vox: torch.Tensor, n_img: int, offset: int = 0, z0: int = 0,
@@ -186,7 +230,7 @@ def moments2d_images(vox: torch.Tensor, imgs: list[torch.Tensor], order: int, of
     """Exact 2D moments (global coordinates) of images made by ``project`` from
     ``vox``; returns the limb accumulator [B, n_img, n2d, 4] (int64 storage of
     uint64 sums), written into ``acc`` when given."""
-    desc = make_desc(vox, offset, z0)
+    desc = make_desc(vox, offset, z0, validate=False)   # the images are already built from vox
     n_img = len(imgs)
     if acc is None:
         acc = torch.empty((desc.B, n_img, n2d(order), 4), dtype=torch.int64, device=vox.device)
@@ -237,8 +281,11 @@ def project_profile(vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0,
     if imgs is None:
         imgs = []
         for k in range(n_img):
-            W, H, _, _ = image_layout(desc, k)
-            imgs.append(None if k == 2 else torch.empty((desc.B, H, W), dtype=torch.int32, device=vox.device))
+            if k == 2:
+                imgs.append(None)
+                continue
+            W, H, _, _ = moments_image_layout(desc, order, k)
+            imgs.append(torch.empty((desc.B, H, W), dtype=torch.int32, device=vox.device))
     if profile is None:
         wq, _, _ = profile_layout(desc, order)
         profile = torch.empty((desc.B, wq), dtype=torch.int64, device=vox.device)
@@ -252,7 +299,7 @@ def moments2d_profile(vox: torch.Tensor, imgs: list[torch.Tensor | None], profil
                       offset: int = 0, z0: int = 0, stream: torch.cuda.Stream | None = None,
                       acc: torch.Tensor | None = None) -> torch.Tensor:
     """DPM_ACC_PROFILE accumulator of ``project_profile`` outputs."""
-    desc = make_desc(vox, offset, z0)
+    desc = make_desc(vox, offset, z0, validate=False)   # the images are already built from vox
     n_img = len(imgs)
     if acc is None:
         acc = torch.empty((desc.B, n_img, n2d(order), 4), dtype=torch.int64, device=vox.device)
@@ -262,14 +309,15 @@ def moments2d_profile(vox: torch.Tensor, imgs: list[torch.Tensor | None], profil
     return acc
 
 
-ACC_KINDS = {"profile": nat.DPM_ACC_PROFILE, "images": nat.DPM_ACC_IMAGES}
+ACC_KINDS = {"profile": nat.DPM_ACC_PROFILE, "profile_t": nat.DPM_ACC_PROFILE_T, "images": nat.DPM_ACC_IMAGES}
 
 
 def derive(acc: torch.Tensor, order: int, stream: torch.cuda.Stream | None = None,
            out: DeviceMoments | None = None, kind: str = "profile") -> DeviceMoments:
     """Device epilogue on a (possibly summed) limb accumulator: ``kind``
-    "profile" for ``moments2d_partial`` / ``moments2d_profile`` accumulators,
-    "images" for ``moments2d_images`` over ``project``'s image set."""
+    ``acc_kind(...)`` ("profile" or "profile_t") for ``moments2d_partial`` /
+    ``moments2d_profile`` accumulators, "images" for ``moments2d_images`` over
+    ``project``'s image set."""
     check_order(order)
     if kind not in ACC_KINDS:
         raise ValueError(f"unknown accumulator kind {kind!r}")
@@ -383,8 +431,12 @@ class GraphedSlabStages:
         dev = vox.device
         self.imgs = []
         for k in range(n_img):
-            W, H, _, _ = image_layout(desc, k)
-            self.imgs.append(None if k == 2 else torch.empty((desc.B, H, W), dtype=torch.int32, device=dev))
+            if k == 2:
+                self.imgs.append(None)
+                continue
+            W, H, _, _ = moments_image_layout(desc, order, k)
+            self.imgs.append(torch.empty((desc.B, H, W), dtype=torch.int32, device=dev))
+        self.kind = acc_kind(vox, order, offset, z0)
         wq, _, _ = profile_layout(desc, order)
         self.profile = torch.empty((desc.B, wq), dtype=torch.int64, device=dev)
         self.acc = torch.empty((desc.B, n_img, n2d(order), 4), dtype=torch.int64, device=dev)
@@ -413,7 +465,7 @@ class GraphedSlabStages:
 
     def _moments2d(self):
         if self.fused:
-            desc = make_desc(self.vox, self.offset, self.z0)
+            desc = make_desc(self.vox, self.offset, self.z0, validate=False)
             ptrs = (ctypes.c_void_p * len(self.imgs))(*[t.data_ptr() if t is not None else None for t in self.imgs])
             nat.check(nat.lib().dpm_moments2d_profile_derive(
                 ctypes.byref(desc), self.order, ptrs, self.profile.data_ptr(), self.acc.data_ptr(),
@@ -423,7 +475,7 @@ class GraphedSlabStages:
             moments2d_profile(self.vox, self.imgs, self.profile, self.order, self.offset, self.z0, acc=self.acc)
 
     def _derive(self):
-        derive(self.acc, self.order, out=self.out)
+        derive(self.acc, self.order, out=self.out, kind=self.kind)
 
     def replay_project(self) -> None:
         self.graphs[0].replay()

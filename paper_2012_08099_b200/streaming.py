@@ -66,7 +66,7 @@ class HostStreamer:
 
     def moments(self, host: torch.Tensor, offset: int = 0):
         acc = self.run(host, offset)
-        res = engine.derive(acc, self.order)
+        res = engine.derive(acc, self.order, kind=engine.acc_kind(self.bufs[0], self.order, offset))
         self.launches += 1
         return res
 
@@ -123,4 +123,4 @@ class FileStreamer:
         return self.acc_total
 
     def moments(self, src):
-        return engine.derive(self.run(src), self.order)
+        return engine.derive(self.run(src), self.order, kind=engine.acc_kind(self.bufs[0], self.order))

@@ -77,3 +77,49 @@ def test_envelope_order6_profile_rule():
     assert lib.dpm_check_envelope(n, n, n, 257, 5) == nat.DPM_OK        # images + profile solve fine at order 5
     assert lib.dpm_check_envelope(n, n, n, 257, 6) == nat.DPM_EOVERFLOW
     assert lib.dpm_check_envelope(n, n, n, 255, 6) == nat.DPM_OK        # just below 2^116
+
+
+def _desc(dims, z0=0, dtype=nat.DPM_U16):
+    d = nat.VolumeDesc()
+    d.L, d.M, d.N = dims
+    d.B = 1
+    d.stride_y, d.stride_z, d.stride_b = dims[0], dims[0] * dims[1], dims[0] * dims[1] * dims[2]
+    d.dtype = dtype
+    d.z0 = z0
+    return d
+
+
+@pytest.mark.parametrize("dims,z0", [((2048, 2048, 256), 1024), ((256, 40, 24), 0), ((264, 9, 150), 17),
+                                     ((203, 11, 13), 0), ((128, 128, 128), 0), ((64, 64, 64), 5)])
+@pytest.mark.parametrize("order", [3, 4, 5, 6])
+def test_moments_layout_geometry(dims, z0, order):
+    """The moments pipeline's image geometry: classic for narrow volumes, layout
+    T (x and z exchanged, slab offset on the x' axis) for L >= 192."""
+    lib = nat.lib()
+    d = _desc(dims, z0)
+    L, M, N = dims
+    kind = lib.dpm_moments_acc_kind(ctypes.byref(d), order)
+    wide = L >= 192
+    assert kind == (nat.DPM_ACC_PROFILE_T if wide else nat.DPM_ACC_PROFILE)
+    for img in range(4 if order <= 3 else order + 1):
+        out = [ctypes.c_int64() for _ in range(4)]
+        rc = lib.dpm_moments_image_layout(ctypes.byref(d), order, img, *[ctypes.byref(o) for o in out])
+        if img == 2:
+            assert rc == nat.DPM_EINVAL
+            continue
+        assert rc == 0
+        got = tuple(o.value for o in out)
+        if not wide:
+            assert got == oracle.layout(dims, img, z0)
+        else:
+            W, H, ai, aj = oracle.layout((N, M, L), img, 0)    # the transposed volume at z0 = 0
+            shift = z0 if img == 0 or img >= 3 else 0          # indices containing x' = z carry the slab offset
+            assert got == (W, H, ai + shift, aj)
+    wq, ai, t = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
+    assert lib.dpm_profile_layout(ctypes.byref(d), order, ctypes.byref(wq), ctypes.byref(ai), ctypes.byref(t)) == 0
+    at = abs(t.value)
+    if wide:
+        assert wq.value == N + at * (L - 1)
+        assert ai.value == (0 if t.value > 0 else -at * (L - 1)) + z0
+    else:
+        assert wq.value == L + at * (N - 1)

@@ -169,7 +169,7 @@ def test_zslab_composition_on_device(cuda):
                 acc = part
             else:
                 engine.acc_add(acc, part)
-        assert _ints(engine.derive(acc, 6)) == whole, splits
+        assert _ints(engine.derive(acc, 6, kind=engine.acc_kind(vol, 6))) == whole, splits
 
 
 def test_cfg5_full_volume_exact(cuda):
@@ -194,6 +194,7 @@ def test_derive_exactness_and_nonexact_flag(cuda, order):
     rng = np.random.default_rng(order)
     vols = rng.integers(0, 65535, size=(2, 13, 11, 17)).astype(np.uint16)
     acc = engine.moments2d_partial(torch.from_numpy(vols).cuda(), order)
+    assert engine.acc_kind(torch.from_numpy(vols), order) == "profile"   # classic layout: slot tags below
     res = engine.derive(acc, order)
     got = res.i128.cpu().numpy()
     idx = vm.moment_indices(order)

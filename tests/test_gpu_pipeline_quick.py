@@ -113,5 +113,5 @@ def test_graphed_slab_stages(cuda, order):
         assert torch.equal(acc, want_acc)
         res = st.replay_derive()
         torch.cuda.synchronize()
-        assert torch.equal(res.i128, engine.derive(want_acc, order).i128)
+        assert torch.equal(res.i128, engine.derive(want_acc, order, kind=engine.acc_kind(slab, order)).i128)
     assert st.launches == 3   # projection, image + profile moments, epilogue

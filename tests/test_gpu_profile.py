@@ -52,16 +52,21 @@ def test_profile_images_and_profile(order, shape, dt):
     vol = rng.integers(0, np.iinfo(dt).max + 1, size=shape).astype(dt)
     v = torch.from_numpy(vol).cuda()
     imgs, prof = engine.project_profile(v, order)
-    ref = engine.project(v, engine.num_images(order))
+    # layout T (wide volumes): the method's images of the volume with x and z exchanged
+    lay_t = engine.acc_kind(v, order) == "profile_t"
+    assert lay_t == (shape[2] >= 192)
+    src = np.ascontiguousarray(vol.transpose(2, 1, 0)) if lay_t else vol
+    ref = engine.project(torch.from_numpy(src).cuda(), engine.num_images(order))
     torch.cuda.synchronize()
     assert imgs[2] is None
     for k in range(engine.num_images(order)):
         if k != 2:
             assert torch.equal(imgs[k], ref[k]), k
+    n, _, l = src.shape
     wq, ai, t = engine.profile_layout(engine.make_desc(v), order)
-    assert t == T_OF_ORDER[order] and wq == shape[2] + abs(t) * (shape[0] - 1)
-    assert ai == (-abs(t) * (shape[0] - 1) if t < 0 else 0)
-    assert np.array_equal(prof[0].cpu().numpy(), np_profile(vol, t))
+    assert t == T_OF_ORDER[order] and wq == l + abs(t) * (n - 1)
+    assert ai == (-abs(t) * (n - 1) if t < 0 else 0)
+    assert np.array_equal(prof[0].cpu().numpy(), np_profile(src, t))
 
 
 @pytest.mark.parametrize("order", [3, 4, 5, 6])
@@ -80,13 +85,14 @@ def test_profile_moments_match_oracle_and_images_route(order, shape, dt):
 def test_profile_zslab_composition(order):
     rng = np.random.default_rng(11)
     vol = rng.integers(0, 65536, size=(70, 20, 256)).astype(np.uint16)
-    whole = _ints(engine.derive(engine.moments2d_partial(torch.from_numpy(vol).cuda(), order), order))
+    kind = engine.acc_kind(torch.from_numpy(vol), order)
+    whole = _ints(engine.derive(engine.moments2d_partial(torch.from_numpy(vol).cuda(), order), order, kind=kind))
     for cuts in ([0, 33, 70], [0, 5, 6, 40, 70]):
         acc = None
         for z0, z1 in zip(cuts[:-1], cuts[1:]):
             part = engine.moments2d_partial(torch.from_numpy(vol[z0:z1]).cuda(), order, z0=z0)
             acc = part.clone() if acc is None else acc + part
-        assert _ints(engine.derive(acc, order)) == whole
+        assert _ints(engine.derive(acc, order, kind=kind)) == whole
 
 
 def test_profile_batch_and_offset():
@@ -104,11 +110,12 @@ def test_profile_fault_injection_is_detected(order, a):
     rng = np.random.default_rng(order)
     vol = rng.integers(0, 65536, size=(24, 16, 256)).astype(np.uint16)
     acc = engine.moments2d_partial(torch.from_numpy(vol).cuda(), order)
-    assert int(engine.derive(acc, order).status[0]) == 0
+    kind = engine.acc_kind(torch.from_numpy(vol), order)
+    assert int(engine.derive(acc, order, kind=kind).status[0]) == 0
     bad = acc.clone()
     p_idx = a * (order + 1) - a * (a - 1) // 2      # idx2(order, a, 0)
     bad[0, 2, p_idx, 0] += 1
-    assert int(engine.derive(bad, order).status[0]) & 1
+    assert int(engine.derive(bad, order, kind=kind).status[0]) & 1
 
 
 def test_profile_graphed_stages_launches():
