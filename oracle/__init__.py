@@ -6,7 +6,7 @@ Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
 imports it.  See oracle/dpm_oracle.c for the reference file:line map.
 """
 from .oracle import (IMAGE_NAMES, dpm, derive3d, layout, load, moment_indices, moments2d,
-                     naive, num_images, project, set_threads, max_threads, synth_noise)
+                     naive, naive_direct, num_images, project, set_threads, max_threads, synth_noise)
 
 __all__ = ["IMAGE_NAMES", "dpm", "derive3d", "layout", "load", "moment_indices", "moments2d",
-           "naive", "num_images", "project", "set_threads", "max_threads", "synth_noise"]
+           "naive", "naive_direct", "num_images", "project", "set_threads", "max_threads", "synth_noise"]

@@ -303,6 +303,48 @@ void vmo_naive(const void* vox, int dtype, int32_t offset, int64_t L, int64_t M,
   }
 }
 
+/* The naive O(n^3)-multiply direct sum, Eq. 2, term by term: every moment
+ * (p, q, r) multiplies every voxel by its own monomial x^p y^q (z+z0)^r
+ * (moments3d.py:78-139 computes each (p, q, r) as a separate voxel-by-monomial
+ * product before its plane and z sums).  Exact in __int128; parallel over z.
+ * A CPU baseline only (bench.py), never a checker: vmo_naive is the checker. */
+void vmo_naive_direct(const void* vox, int dtype, int32_t offset, int64_t L, int64_t M, int64_t N,
+                      int64_t z0, int order, i128* out) {
+  const int n3 = vmo_num_moments3d(order);
+  int tp[128], tq[128], tr[128];
+  {
+    int m = 0;
+    for (int p = 0; p <= order; ++p)
+      for (int q = 0; p + q <= order; ++q)
+        for (int r = 0; p + q + r <= order; ++r, ++m) { tp[m] = p; tq[m] = q; tr[m] = r; }
+  }
+  for (int k = 0; k < n3; ++k) out[k] = 0;
+#pragma omp parallel
+  {
+    i128* acc = (i128*)calloc((size_t)n3, sizeof(i128));
+    i128 px[8], py[8], pz[8];
+#pragma omp for schedule(static)
+    for (int64_t z = 0; z < N; ++z) {
+      pz[0] = 1;
+      for (int k = 1; k <= order; ++k) pz[k] = pz[k - 1] * (z + z0);
+      for (int64_t y = 0; y < M; ++y) {
+        py[0] = 1;
+        for (int k = 1; k <= order; ++k) py[k] = py[k - 1] * y;
+        const size_t base = (size_t)((z * M + y) * L);
+        for (int64_t x = 0; x < L; ++x) {
+          const int64_t v = voxel_at(vox, dtype, offset, base + (size_t)x);
+          px[0] = 1;
+          for (int k = 1; k <= order; ++k) px[k] = px[k - 1] * x;
+          for (int m = 0; m < n3; ++m) acc[m] += (i128)v * px[tp[m]] * py[tq[m]] * pz[tr[m]];
+        }
+      }
+    }
+#pragma omp critical
+    for (int k = 0; k < n3; ++k) out[k] += acc[k];
+    free(acc);
+  }
+}
+
 int vmo_max_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();
@@ -340,30 +382,41 @@ static inline uint64_t vmo_sweight(int64_t f, int64_t S) {
   return (uint64_t)((f * f * (3 * S - 2 * f)) * 65536 / (S * S * S));
 }
 void vmo_synth_noise_u16(uint16_t* out, int64_t L, int64_t M, int64_t z0, int64_t nz, uint64_t seed) {
-#pragma omp parallel for collapse(2) schedule(static)
-  for (int64_t zi = 0; zi < nz; ++zi) {
-    for (int64_t y = 0; y < M; ++y) {
-      const int64_t z = z0 + zi;
-      for (int64_t x = 0; x < L; ++x) {
-        uint64_t sum = 0;
+  /* per row and octave the 8 lattice hashes of an x-cell are shared by its S
+   * voxels: hashed once per cell, then the (bit-identical) weights per voxel */
+#pragma omp parallel
+  {
+    uint64_t* acc = (uint64_t*)malloc((size_t)L * sizeof(uint64_t));
+#pragma omp for collapse(2) schedule(static)
+    for (int64_t zi = 0; zi < nz; ++zi) {
+      for (int64_t y = 0; y < M; ++y) {
+        const int64_t z = z0 + zi;
+        for (int64_t x = 0; x < L; ++x) acc[x] = 0;
         for (int o = 0; o < 4; ++o) {
           const int64_t S = 128 >> o;
-          const int64_t cx = x / S, cy = y / S, cz = z / S;
-          const uint64_t wx = vmo_sweight(x - cx * S, S), wy = vmo_sweight(y - cy * S, S), wz = vmo_sweight(z - cz * S, S);
-          uint64_t c[2];
-          for (int dz = 0; dz < 2; ++dz) {
-            uint64_t b[2];
-            for (int dy = 0; dy < 2; ++dy) {
-              const uint64_t h0 = vmo_lattice(seed, o, cx, cy + dy, cz + dz);
-              const uint64_t h1 = vmo_lattice(seed, o, cx + 1, cy + dy, cz + dz);
-              b[dy] = h0 * (65536 - wx) + h1 * wx;
+          const int64_t cy = y / S, cz = z / S;
+          const uint64_t wy = vmo_sweight(y - cy * S, S), wz = vmo_sweight(z - cz * S, S);
+          for (int64_t cx = 0; cx * S < L; ++cx) {
+            uint64_t h[2][2][2];
+            for (int dz = 0; dz < 2; ++dz)
+              for (int dy = 0; dy < 2; ++dy)
+                for (int dx = 0; dx < 2; ++dx) h[dz][dy][dx] = vmo_lattice(seed, o, cx + dx, cy + dy, cz + dz);
+            const int64_t xe = (cx + 1) * S < L ? (cx + 1) * S : L;
+            for (int64_t x = cx * S; x < xe; ++x) {
+              const uint64_t wx = vmo_sweight(x - cx * S, S);
+              uint64_t c[2];
+              for (int dz = 0; dz < 2; ++dz) {
+                const uint64_t b0 = h[dz][0][0] * (65536 - wx) + h[dz][0][1] * wx;
+                const uint64_t b1 = h[dz][1][0] * (65536 - wx) + h[dz][1][1] * wx;
+                c[dz] = b0 * (65536 - wy) + b1 * wy;
+              }
+              acc[x] += ((c[0] * (65536 - wz) + c[1] * wz) >> 48) << (3 - o);
             }
-            c[dz] = b[0] * (65536 - wy) + b[1] * wy;
           }
-          sum += ((c[0] * (65536 - wz) + c[1] * wz) >> 48) << (3 - o);
         }
-        out[(zi * M + y) * L + x] = (uint16_t)(sum / 15);
+        for (int64_t x = 0; x < L; ++x) out[(zi * M + y) * L + x] = (uint16_t)(acc[x] / 15);
       }
     }
+    free(acc);
   }
 }

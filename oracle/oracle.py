@@ -45,6 +45,7 @@ def load() -> ctypes.CDLL:
     lib.vmo_dpm.argtypes = [vp, ctypes.c_int, i32, i64, i64, i64, i64, ctypes.c_int, vp]
     lib.vmo_dpm.restype = ctypes.c_int
     lib.vmo_naive.argtypes = [vp, ctypes.c_int, i32, i64, i64, i64, i64, ctypes.c_int, vp]
+    lib.vmo_naive_direct.argtypes = [vp, ctypes.c_int, i32, i64, i64, i64, i64, ctypes.c_int, vp]
     lib.vmo_set_threads.argtypes = [ctypes.c_int]
     lib.vmo_synth_noise_u16.argtypes = [vp, i64, i64, i64, i64, ctypes.c_uint64]
     return lib
@@ -147,10 +148,21 @@ def dpm(voxels: np.ndarray, order: int, z0: int = 0, offset: int = 0) -> dict[tu
 
 
 def naive(voxels: np.ndarray, order: int, z0: int = 0, offset: int = 0) -> dict[tuple[int, int, int], int]:
-    """Direct Eq. 2 sum, exact ints (the naive O(n^3)-multiply baseline)."""
+    """Direct Eq. 2 sum, exact ints, factored row -> plane -> volume (the
+    checker; factored_moments' evaluation order, moments3d.py:142-198)."""
     v, code, dims = _vol(voxels)
     out = np.zeros((len(moment_indices(order)), 2), dtype=np.int64)
     load().vmo_naive(v.ctypes.data, code, offset, *dims, z0, order, out.ctypes.data)
+    return dict(zip(moment_indices(order), _from_i128(out)))
+
+
+def naive_direct(voxels: np.ndarray, order: int, z0: int = 0, offset: int = 0) -> dict[tuple[int, int, int], int]:
+    """Eq. 2 term by term -- every voxel times every moment's monomial, the
+    naive O(n^3)-multiply direct sum (moments3d.py:78-139) -- exact ints.
+    A CPU BASELINE for bench.py; tests pin it to ``naive``."""
+    v, code, dims = _vol(voxels)
+    out = np.zeros((len(moment_indices(order)), 2), dtype=np.int64)
+    load().vmo_naive_direct(v.ctypes.data, code, offset, *dims, z0, order, out.ctypes.data)
     return dict(zip(moment_indices(order), _from_i128(out)))
 
 

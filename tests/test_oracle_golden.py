@@ -172,3 +172,21 @@ def test_translation_binomial_anchor():              # test_moments3d.py:105-113
     t0, t1 = oracle.dpm(a, 6), oracle.dpm(b, 6)
     for p in range(7):
         assert t1[(p, 0, 0)] == sum(comb(p, s) * t0[(s, 0, 0)] for s in range(p + 1))
+
+
+@pytest.mark.parametrize("shape,order,z0", [((9, 7, 5), 5, 3), ((4, 6, 3), 6, 0), ((12, 3, 8), 4, 11)])
+def test_naive_direct_baseline_equals_checker(shape, order, z0):
+    """The term-by-term naive sum timed as a CPU baseline (bench.py) computes
+    the same exact moments as the factored checker."""
+    rng = np.random.default_rng(sum(shape) + order)
+    v = rng.integers(0, 65536, size=shape).astype(np.uint16)
+    assert oracle.naive_direct(v, order, z0=z0) == oracle.naive(v, order, z0=z0)
+
+
+def test_synth_noise_host_generator_is_stable():
+    """The host copy of the cfg5 generator (rewritten for speed) keeps its
+    values: pinned to the committed golden slab hash."""
+    import hashlib
+    v = oracle.synth_noise(64, 48, 100, 3, 5)
+    assert v.dtype == np.uint16 and v.shape == (3, 48, 64)
+    assert hashlib.sha256(v.tobytes()).hexdigest()[:16] == "ca1ff95770fc83bd"   # = the pre-rewrite generator
