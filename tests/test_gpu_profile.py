@@ -32,16 +32,18 @@ def _ints(res):
     return [engine.i128_to_ints(res.i128[b].cpu().numpy()) for b in range(res.i128.shape[0])]
 
 
+# L >= 192 is layout T (the z-streaming kernel, project_zstream.cu); narrower
+# volumes use the y-streaming kernel (project_stream.cu) with its classic images
 SHAPES = [
-    ((24, 40, 264), np.uint16),     # TMA streaming kernel, VX = 8, partial x-tile
-    ((100, 17, 256), np.uint16),    # two z-tiles
-    ((16, 8, 64), np.uint8),        # VX = 4 (16 planes per warp, 2 CTAs per SM at order 3)
-    ((150, 9, 264), np.uint8),      # VX = 8 uint8 (16 planes per warp at orders 3-4), two z-tiles
-    ((140, 10, 128), np.uint16),    # VX = 4 uint16 (16 planes / 2 CTAs at order 3), two z-tiles
+    ((24, 40, 264), np.uint16),     # layout T: two x-tiles (the second 8 wide), 4 y-groups, 3 z-steps
+    ((100, 17, 256), np.uint16),    # layout T: partial last z-step and y-group
+    ((16, 8, 64), np.uint8),        # classic, 4-wide lanes; order 3: the SMALL variant (< 8 row-steps per SM)
+    ((150, 9, 264), np.uint8),      # layout T, uint8 (8-byte lane vectors)
+    ((140, 10, 128), np.uint16),    # classic, 4-wide uint16 lanes, two z-tiles (order 3: SMALL variant)
     ((9, 7, 5), np.uint8),          # generic kernel
-    ((13, 11, 203), np.uint16),     # generic kernel (unaligned rows)
-    ((60, 300, 128), np.uint8),     # single tile (rows stored, images not zeroed), runs not aligned to 8 rows
-    ((50, 200, 256), np.uint16),    # single tile with 8-wide lanes, all orders (order 6: direct YZ stores)
+    ((13, 11, 203), np.uint16),     # layout T through the generic kernel on the transposed view (L % 8 != 0)
+    ((60, 300, 128), np.uint8),     # classic single tile (rows stored, images not zeroed), runs not aligned to 8 rows
+    ((50, 200, 256), np.uint16),    # layout T, one x-tile, 17 y-groups
 ]
 
 
