@@ -373,7 +373,7 @@ def main():
         graphed = engine.GraphedMoments(vox, order, offset=offset)   # captured once, replayed per step
     else:
         # three graphs with the all-reduce between; one device: the epilogue rides the moments launch
-        stages = engine.GraphedSlabStages(vox, order, offset=offset, z0=z0, fused=(world == 1))
+        stages = engine.GraphedSlabStages(vox, order, offset=offset, z0=z0, fused=(world == 1), n_global=n_global)
 
     def step(i=None):
         if cfg == 5:
@@ -503,7 +503,7 @@ def simulate_ranks(args, dev):
         for r in range(g):
             z0, z1 = pdist.slab_bounds(N, g, r)
             slab = engine.synth_noise(L, M, z0, z1 - z0, CFG5_SEED, device=dev)
-            st = engine.GraphedSlabStages(slab, 6, z0=z0, fused=False)
+            st = engine.GraphedSlabStages(slab, 6, z0=z0, fused=False, n_global=N)
             for _ in range(max(3, args.warmup)):
                 st.replay_project(); st.replay_moments2d(); st.replay_derive()
             torch.cuda.synchronize()

@@ -1,4 +1,6 @@
-// ptx.cuh -- thin inline-PTX helpers for sm_100a (TMA, mbarrier, shared/global reductions).
+// ptx.cuh -- thin inline-PTX helpers for sm_100a: TMA loads, mbarriers,
+// shared/global reductions and 32-bit shared-memory accesses.  Only what the
+// kernels use (project_stream.cu, project_zstream.cu).
 #pragma once
 #include <cstdint>
 #include <cuda.h>
@@ -10,11 +12,59 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// red.shared.add.u32 [addr + OFF], v   (no return value, no branch)
-template <int OFF>
-__device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
-  asm volatile("red.shared.add.u32 [%0+%1], %2;" ::"r"(addr), "n"(OFF), "r"(v) : "memory");
+// ---- mbarriers ---------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
 }
+
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_addr(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// spin until the phase with parity `phase` of the barrier at shared address `bar` completed
+__device__ __forceinline__ void mbar_wait_addr(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n"
+      "WAITA_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra WAITA_%=;\n\t}" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+
+// ---- TMA -----------------------------------------------------------------------
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// 4-D tiled TMA load global -> shared with an L2 cache policy, completion
+// counted on an mbarrier
+__device__ __forceinline__ void tma_load_4d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                                 int32_t c1, int32_t c2, int32_t c3, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(bar)), "l"(policy)
+      : "memory");
+}
+
+// ---- reductions -------------------------------------------------------------------
+// red.shared.add.u32 [addr], v   (no return value)
 __device__ __forceinline__ void red_shared_add_dyn(uint32_t addr, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
@@ -29,208 +79,13 @@ __device__ __forceinline__ void red_global_add_if(uint32_t* gptr, uint32_t v, bo
       : "memory");
 }
 
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void fence_barrier_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-__device__ __forceinline__ void fence_proxy_async_shared() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n\t.reg .pred done;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
-      "@!done bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
-      "r"(phase)
-      : "memory");
-}
-
-// 4D tiled TMA load global -> shared, completion counted on an mbarrier
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
-                                            int32_t c1, int32_t c2, int32_t c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_addr(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
-  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
-
-}  // namespace ptx
-}  // namespace dpm
-
-namespace dpm {
-namespace ptx {
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-}  // namespace ptx
-}  // namespace dpm
-
-namespace dpm {
-namespace ptx {
-__device__ __forceinline__ void mbar_wait_addr(uint32_t bar, uint32_t phase) {
-  asm volatile(
-      "{\n\t.reg .pred done;\n"
-      "WAITA_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
-      "@!done bra WAITA_%=;\n\t}" ::"r"(bar),
-      "r"(phase)
-      : "memory");
-}
-}  // namespace ptx
-}  // namespace dpm
-
-namespace dpm {
-namespace ptx {
-__device__ __forceinline__ bool mbar_test_addr(uint32_t bar, uint32_t phase) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok) : "r"(bar), "r"(phase) : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_arrive_addr(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t d;
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
-}  // namespace ptx
-}  // namespace dpm
-
-namespace dpm {
-namespace ptx {
-// acc += value of lane (lane - delta) if that lane exists (shfl.up with the in-range predicate)
-__device__ __forceinline__ uint32_t add_from_lane_below(uint32_t acc, uint32_t v, int delta) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t.reg .b32 r;\n\t"
-      "shfl.sync.up.b32 r|p, %1, %2, 0, 0xffffffff;\n\t"
-      "@p add.u32 %0, %0, r;\n\t}"
-      : "+r"(acc) : "r"(v), "r"(delta));
-  return acc;
-}
-}  // namespace ptx
-}  // namespace dpm
-
-namespace dpm {
-namespace ptx {
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void tma_load_4d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
-                                                 int32_t c1, int32_t c2, int32_t c3, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_addr(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(bar)), "l"(policy)
-      : "memory");
-}
-}  // namespace ptx
-}  // namespace dpm
-
-namespace dpm {
-namespace ptx {
-__device__ __forceinline__ uint32_t mulhi_u32(uint32_t a, uint32_t b) {
-  uint32_t d;
-  asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
-  return d;
-}
-}  // namespace ptx
-}  // namespace dpm
-
-namespace dpm {
-namespace ptx {
-// value of lane (lane - delta), or 0 where that lane does not exist (shfl.up + in-range predicate)
-__device__ __forceinline__ uint32_t from_lane_below(uint32_t v, int delta) {
-  uint32_t out;
-  asm("{\n\t.reg .pred p;\n\t.reg .b32 r;\n\t"
-      "shfl.sync.up.b32 r|p, %1, %2, 0, 0xffffffff;\n\t"
-      "selp.b32 %0, r, 0, p;\n\t}"
-      : "=r"(out) : "r"(v), "r"(delta));
-  return out;
-}
-}  // namespace ptx
-}  // namespace dpm
-
-// ---- tcgen05 / TMEM (sm_100a) -----------------------------------------------
-namespace dpm {
-namespace ptx {
-// one warp: allocate `ncols` TMEM columns (power of 2 >= 32); the base address is written to smem
-__device__ __forceinline__ void tmem_alloc(uint32_t smem_dst, uint32_t ncols) {
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_dst), "r"(ncols) : "memory");
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-// D[tmem] (+)= A[smem] x B[smem], kind::i8 (int32 accumulate), issued by one thread
-__device__ __forceinline__ void mma_i8(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// arrive on an mbarrier when all previously issued tcgen05.mma of this thread complete
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-}
-// 32 consecutive TMEM columns of this warp's 32 lanes -> 32 registers per thread
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-// shared-memory matrix descriptor (sm100 UMMA): addresses/offsets in bytes
-__host__ __device__ __forceinline__ uint64_t umma_desc(uint32_t smem_addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
-  return (uint64_t)((smem_addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | ((uint64_t)layout << 61);
-}
-}  // namespace ptx
-}  // namespace dpm
-
-namespace dpm {
-namespace ptx {
 // red.global.add.u32 [gptr + OFF] (unconditional; OFF in bytes)
 template <int OFF>
 __device__ __forceinline__ void red_global_add_off(uint32_t* gptr, uint32_t v) {
   asm volatile("red.global.add.u32 [%0+%1], %2;" ::"l"(gptr), "n"(OFF), "r"(v) : "memory");
 }
-// st.global.u32 [gptr + OFF] (rows a single CTA completes: no read-modify-write)
-template <int OFF>
-__device__ __forceinline__ void st_global_off(uint32_t* gptr, uint32_t v) {
-  asm volatile("st.global.u32 [%0+%1], %2;" ::"l"(gptr), "n"(OFF), "r"(v) : "memory");
-}
+
+// predicated st.global.u32 (rows a single CTA completes: no read-modify-write)
 __device__ __forceinline__ void st_global_if(uint32_t* gptr, uint32_t v, bool pred) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -239,11 +94,16 @@ __device__ __forceinline__ void st_global_if(uint32_t* gptr, uint32_t v, bool pr
       "r"(v), "r"((uint32_t)pred)
       : "memory");
 }
-}  // namespace ptx
-}  // namespace dpm
 
-namespace dpm {
-namespace ptx {
+// ---- arithmetic -----------------------------------------------------------------
+// a * b + c on the FMA pipe (b is a run-time 1 for the IMAD-by-1 folds)
+__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// ---- 32-bit shared-memory addresses ------------------------------------------------
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
@@ -252,16 +112,19 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
 __device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
+// stage loads: volatile (ordered after the mbarrier wait) but no memory clobber,
+// so the fold arithmetic around them schedules freely
 template <typename V> __device__ __forceinline__ V lds_vec(uint32_t addr);
 template <> __device__ __forceinline__ uint4 lds_vec<uint4>(uint32_t addr) {
   uint4 v;
-  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr) : "memory");
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
   return v;
 }
 template <> __device__ __forceinline__ uint2 lds_vec<uint2>(uint32_t addr) {
   uint2 v;
-  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr) : "memory");
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
   return v;
 }
+
 }  // namespace ptx
 }  // namespace dpm

@@ -56,7 +56,7 @@ def moments_zslab(slab: torch.Tensor, order: int, z0: int, n_global: int, offset
     engine.check_order(order)
     d = engine.make_desc(slab, offset, z0)
     engine.check_envelope(d.L, d.M, n_global, d.dtype, order)
-    acc = engine.moments2d_partial(slab, order, offset=offset, z0=z0, stream=stream)
+    acc = engine.moments2d_partial(slab, order, offset=offset, z0=z0, stream=stream, n_global=n_global)
     allreduce_limbs(acc, group)
     return engine.derive(acc, order, stream=stream, kind=engine.acc_kind(slab, order, offset, z0))
 

@@ -250,13 +250,16 @@ def profile_layout(desc: nat.VolumeDesc, order: int) -> tuple[int, int, int]:
 
 def moments2d_partial(vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0,
                       stream: torch.cuda.Stream | None = None, acc: torch.Tensor | None = None,
-                      workspace: torch.Tensor | None = None) -> torch.Tensor:
+                      workspace: torch.Tensor | None = None, n_global: int | None = None) -> torch.Tensor:
     """The moments pipeline's projection pass + exact moments of a slab in
-    GLOBAL coordinates (dpm_moments_partial); returns the DPM_ACC_PROFILE limb
-    accumulator [B, n_img, n2d, 4].  Accumulators of z-slabs add elementwise
-    (moments are linear in the voxels); finish with ``derive(acc, order)``."""
+    GLOBAL coordinates (dpm_moments_partial); returns the limb accumulator
+    [B, n_img, n2d, 4] of kind ``acc_kind(vox, order)``.  Accumulators of
+    z-slabs add elementwise (moments are linear in the voxels); finish with
+    ``derive(acc, order, kind=...)``.  ``n_global``: planes of the whole
+    volume (default z0 + N), checked against the exactness envelope."""
     check_order(order)
     desc = make_desc(vox, offset, z0)
+    check_envelope(desc.L, desc.M, n_global if n_global is not None else desc.z0 + desc.N, desc.dtype, order)
     lib = nat.lib()
     wsb = int(lib.dpm_partial_workspace_bytes(ctypes.byref(desc), order))
     if wsb == 0:
@@ -419,14 +422,23 @@ class GraphedSlabStages:
     multi-GPU caller all-reduces ``acc`` between (2) and (3) (the exchange is
     not captured).  Replays are issued on the caller's current stream."""
 
-    def __init__(self, vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0, fused: bool = False):
+    def __init__(self, vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0, fused: bool = False,
+                 n_global: int | None = None):
         """``fused``: single device, no exchange between (2) and (3): stage 2
         ends with the epilogue in the same launch and ``replay_derive`` only
-        returns ``out``."""
+        returns ``out`` -- refused inside a multi-rank process group, where
+        the limbs must be all-reduced BEFORE the epilogue.  ``n_global``:
+        planes of the whole volume (default z0 + N), checked against the
+        exactness envelope."""
         check_order(order)
+        if fused and torch.distributed.is_available() and torch.distributed.is_initialized() \
+                and torch.distributed.get_world_size() > 1:
+            raise ValueError("fused=True runs the epilogue before any exchange: use fused=False (replay_moments2d, "
+                             "all-reduce, replay_derive) inside a multi-rank process group")
         self.vox, self.order, self.offset, self.z0 = vox, order, offset, z0
         self.fused = fused
         desc = make_desc(vox, offset, z0)
+        check_envelope(desc.L, desc.M, n_global if n_global is not None else desc.z0 + desc.N, desc.dtype, order)
         n_img = num_images(order)
         dev = vox.device
         self.imgs = []
@@ -481,6 +493,8 @@ class GraphedSlabStages:
         self.graphs[0].replay()
 
     def replay_moments2d(self) -> torch.Tensor:
+        """Exact 2D moments into ``acc`` (with ``fused`` the epilogue already
+        ran in the same launch: ``acc`` is then final, not for an exchange)."""
         self.graphs[1].replay()
         return self.acc
 

@@ -11,6 +11,7 @@ both (L+2N-2) x M -- available through ``project_extended``.
 from __future__ import annotations
 
 import enum
+import threading
 import warnings
 from dataclasses import dataclass
 
@@ -112,18 +113,22 @@ class _Uploader:
     """Host -> device copies of large pageable volumes: plane chunks are copied
     by a thread pool (numpy releases the GIL) into two pinned staging buffers
     while the other buffer's H2D runs on a copy stream -- ~2-3x the driver's
-    pageable copy rate.  One per process, created lazily."""
+    pageable copy rate.  One per (device, calling thread) -- the staging
+    buffers, the copy stream and its events are never shared between
+    concurrent callers -- created lazily by ``_uploader()``."""
 
     CHUNK = 64 << 20
     THREADS = 8
 
-    def __init__(self):
+    def __init__(self, device):
         import torch
         from concurrent.futures import ThreadPoolExecutor
 
+        self.device = torch.device(device)
         self.stage = [torch.empty(self.CHUNK, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
-        self.done = [torch.cuda.Event() for _ in range(2)]
-        self.stream = torch.cuda.Stream()
+        with torch.cuda.device(self.device):
+            self.done = [torch.cuda.Event() for _ in range(2)]
+            self.stream = torch.cuda.Stream(device=self.device)
         self.pool = ThreadPoolExecutor(self.THREADS)
 
     def upload(self, arr: np.ndarray):
@@ -134,8 +139,8 @@ class _Uploader:
         per = max(1, self.CHUNK // plane)
         if per * plane > self.CHUNK or plane > self.CHUNK:
             return None                                   # planes larger than a chunk: caller's fallback
-        dev = torch.empty(arr.shape, dtype=_torch_dtypes()[arr.dtype], device="cuda")
-        self.stream.wait_stream(torch.cuda.current_stream())
+        dev = torch.empty(arr.shape, dtype=_torch_dtypes()[arr.dtype], device=self.device)
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
         for k, z0 in enumerate(range(0, n, per)):
             z1 = min(n, z0 + per)
             i = k % 2
@@ -148,23 +153,33 @@ class _Uploader:
                 dev[z0:z1].copy_(self.stage[i][: (z1 - z0) * plane].view(dev.dtype).view(dev[z0:z1].shape),
                                  non_blocking=True)
                 self.done[i].record(self.stream)
-        torch.cuda.current_stream().wait_stream(self.stream)
+        torch.cuda.current_stream(self.device).wait_stream(self.stream)
         return dev
 
 
-_UPLOADER = None
+_UPLOADERS: dict = {}
+_UPLOADERS_LOCK = threading.Lock()
+
+
+def _uploader():
+    """This thread's uploader for the current CUDA device."""
+    import torch
+
+    key = (torch.cuda.current_device(), threading.get_ident())
+    with _UPLOADERS_LOCK:
+        up = _UPLOADERS.get(key)
+        if up is None:
+            up = _UPLOADERS[key] = _Uploader(torch.device("cuda", key[0]))
+        return up
 
 
 def _to_device(volume):
     import torch
 
-    global _UPLOADER
     if isinstance(volume, Volume):
         arr = np.ascontiguousarray(volume.voxels)
         if arr.nbytes >= (32 << 20) and arr.ndim == 3:
-            if _UPLOADER is None:
-                _UPLOADER = _Uploader()
-            dev = _UPLOADER.upload(arr)
+            dev = _uploader().upload(arr)
             if dev is not None:
                 return dev
         with warnings.catch_warnings():   # read-only voxels are only read (copied to the device), never written

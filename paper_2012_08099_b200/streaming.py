@@ -37,6 +37,7 @@ class HostStreamer:
         global plane ``z_base`` of a volume with ``n_global`` planes."""
         assert tuple(host.shape) == (self.N, self.M, self.L) and host.dtype == self.dtype
         n_global = n_global if n_global is not None else z_base + self.N
+        engine.check_envelope(self.L, self.M, n_global, engine._TORCH_DTYPE[self.dtype], self.order)
         comp = torch.cuda.current_stream(self.device)
         self.acc_total.zero_()
         self.launches = 1
@@ -50,7 +51,7 @@ class HostStreamer:
             i = k % 2
             comp.wait_event(self.copied[i])
             slab = self.bufs[i][: z1 - z0]
-            acc = engine.moments2d_partial(slab, self.order, offset=offset, z0=z_base + z0)
+            acc = engine.moments2d_partial(slab, self.order, offset=offset, z0=z_base + z0, n_global=n_global)
             self.launches += 2
             engine.acc_add(self.acc_total, acc)
             self.launches += 1
@@ -103,6 +104,7 @@ class FileStreamer:
     def run(self, src) -> torch.Tensor:
         """Limb accumulator of the 2D moments of ``src`` ([N, M, L] array)."""
         assert tuple(src.shape) == (self.N, self.M, self.L)
+        engine.check_envelope(self.L, self.M, self.N, engine._TORCH_DTYPE[self.bufs[0].dtype], self.order)
         comp = torch.cuda.current_stream(self.device)
         self.acc_total.zero_()
         self.bytes_read = 0
@@ -117,7 +119,7 @@ class FileStreamer:
                 self.bufs[i][: z1 - z0].copy_(self.staging[i][: z1 - z0], non_blocking=True)
                 self.copied[i].record(self.copy_stream)
             comp.wait_event(self.copied[i])
-            acc = engine.moments2d_partial(self.bufs[i][: z1 - z0], self.order, z0=z0)
+            acc = engine.moments2d_partial(self.bufs[i][: z1 - z0], self.order, z0=z0, n_global=self.N)
             engine.acc_add(self.acc_total, acc)
             self.consumed[i].record(comp)
         return self.acc_total

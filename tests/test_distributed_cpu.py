@@ -77,3 +77,71 @@ def test_slab_and_batch_bounds_cover_exactly():
     assert pdist.batch_bounds(1024, 8, 3) == (384, 512)
     with pytest.raises(ValueError):
         pdist.slab_bounds(10, 2, 2)
+
+
+def _gather_worker(rank, world, port, counts, q):
+    """moments_batch_sharded(gather=True) with a CPU stand-in for the device
+    engine (engine.moments replaced by the oracle): uneven shards are padded,
+    all-gathered and trimmed back in rank order."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2012_08099_b200.engine import DeviceMoments
+        rng = np.random.default_rng(100)
+        vols = rng.integers(0, 256, (sum(counts), 5, 4, 6), dtype=np.uint8)
+        b0 = sum(counts[:rank])
+        mine = torch.from_numpy(vols[b0:b0 + counts[rank]])
+
+        def cpu_moments(v, order, offset=0, **_):
+            rows = [[float(x) for x in oracle.dpm(v[b].numpy(), order).values()] for b in range(v.shape[0])]
+            f64 = torch.tensor(rows, dtype=torch.float64).reshape(v.shape[0], -1)
+            return DeviceMoments(i128=None, f64=f64, status=torch.zeros(v.shape[0], dtype=torch.int32), launches=0)
+        engine.moments = cpu_moments
+        res, gathered = pdist.moments_batch_sharded(mine, 3, gather=True)
+        q.put((rank, gathered.numpy().tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_batch_sharded_gather_world2():
+    counts = [3, 2]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 2, port, counts, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(60)
+    rng = np.random.default_rng(100)
+    vols = rng.integers(0, 256, (5, 5, 4, 6), dtype=np.uint8)
+    want = [[float(x) for x in oracle.dpm(vols[b], 3).values()] for b in range(5)]
+    assert out[0] == want and out[1] == want
+
+
+def _fused_guard_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        try:
+            engine.GraphedSlabStages(torch.zeros((8, 4, 256), dtype=torch.uint16), 4, fused=True)
+            q.put((rank, "no error"))
+        except ValueError as exc:
+            q.put((rank, "ValueError" if "fused" in str(exc) else str(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_slab_stages_refused_in_a_multirank_group():
+    """fused=True would run the epilogue before the limb all-reduce."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fused_guard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(60)
+    assert out == {0: "ValueError", 1: "ValueError"}

@@ -192,3 +192,23 @@ def test_graphed_slab_stages_fused_epilogue(order):
         fused.replay_project(); fused.replay_moments2d(); b = fused.replay_derive()
         torch.cuda.synchronize()
         assert torch.equal(a.i128, b.i128) and torch.equal(a.status, b.status) and int(b.status[0]) == 0
+
+
+def test_public_api_upload_is_thread_safe():
+    """Two threads calling dpm_moments at once on >= 32 MB volumes: each gets its
+    own pinned staging buffers and copy stream (projection._uploader), so the
+    results are exact for both."""
+    from concurrent.futures import ThreadPoolExecutor
+    rng = np.random.default_rng(31)
+    vols = [rng.integers(0, 65536, size=(160, 256, 512), dtype=np.uint16) for _ in range(2)]   # 40 MB each
+    want = [vm.dpm_moments(vm.Volume(v), 4).values for v in vols]
+
+    def run(i):
+        out = []
+        for _ in range(3):
+            out.append(vm.dpm_moments(vm.Volume(vols[i]), 4).values)
+        return out
+    with ThreadPoolExecutor(2) as ex:
+        got = list(ex.map(run, range(2)))
+    for i in range(2):
+        assert all(g == want[i] for g in got[i]), i

@@ -112,3 +112,19 @@ def test_moments2d_type_mirrors_reference():
     from paper_2012_08099_b200.drt2d import Moments2D
     m = Moments2D(3, {(0, 0): 7, (1, 0): 3}, 2)
     assert m[(1, 0)] == 3 and m.mass == 7 and m.origin_offset == 2
+
+
+def test_int16_offset_range_is_validated():
+    """int16 + offset must land in 0..65535 (exact uint32 ray sums): a negative
+    voxel without an offset, or an offset pushing values past 65535, is
+    refused before any device work; unsigned voxels take no offset."""
+    ok = torch.tensor([[[-1024, 3071]]], dtype=torch.int16)
+    engine.make_desc(ok, offset=1024)
+    with pytest.raises(ValueError, match="outside 0..65535"):
+        engine.make_desc(ok, offset=0)
+    with pytest.raises(ValueError, match="outside 0..65535"):
+        engine.make_desc(torch.tensor([[[30000]]], dtype=torch.int16), offset=40000)
+    with pytest.raises(ValueError, match="int16 input only"):
+        engine.make_desc(torch.zeros((2, 2, 2), dtype=torch.uint16), offset=5)
+    with pytest.raises(ValueError):
+        engine.make_desc(ok, offset=200000)
