@@ -228,6 +228,18 @@ DPM_API int dpm_synth_noise_u16(uint16_t* d_out, int64_t L, int64_t M, int64_t z
 /* Number of kernels the last dpm_* call on this thread enqueued (bench evidence). */
 DPM_API int dpm_last_launch_count(void);
 
+/* ---- the reference's direct engines (cross-checks, not the hot path) ------
+ * Exact Eq. 2 sums M_pqr = sum V x^p y^q (z + z0)^r on the device, the
+ * counterparts of naive_moments (moments3d.py:78-139: every voxel times every
+ * in-plane monomial) and factored_moments (moments3d.py:142-198: x-rows, then
+ * y-slices, then z).  `method`: DPM_DIRECT_NAIVE or DPM_DIRECT_FACTORED.
+ * d_ws: dpm_direct_workspace_bytes() of scratch (per-plane limb sums). */
+#define DPM_DIRECT_NAIVE 0
+#define DPM_DIRECT_FACTORED 1
+DPM_API size_t dpm_direct_workspace_bytes(const dpm_volume_desc* desc, int order);
+DPM_API int dpm_direct_moments(const dpm_volume_desc* desc, const void* d_voxels, int order, int method,
+                               void* d_ws, size_t ws_bytes, int64_t* d_m3d_i128, double* d_m3d_f64, void* stream);
+
 DPM_API const char* dpm_strerror(int code);
 
 #ifdef __cplusplus

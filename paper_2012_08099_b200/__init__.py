@@ -14,7 +14,7 @@ from .errors import FormatError, InconsistencyError
 from .features import (CentralMoments3, ShapeFeatures, apply_spacing, central_moments, centroid, feature_report,
                        normalize_scale, shape_features)
 from .moments3d import (ENGINES, MomentTensor3, count_ops, dpm_generic_moments, dpm_moments, dpm_moments_batch,
-                        dpm_moments_file, moment_indices)
+                        dpm_moments_file, factored_moments, moment_indices, naive_moments)
 from .projection import (ANGLES, Orientation, ProjectionImage, ProjectionSet, project, project_all,
                          project_extended, project_subset, write_pgm)
 from .volio import VolumeMeta, load_nrrd, load_raw, meta_from_header_file, open_nrrd, open_raw, write_raw
@@ -26,7 +26,7 @@ __all__ = [
     "ANGLES", "BenchReport", "CentralMoments3", "ENGINES", "FormatError", "ShapeFeatures", "apply_spacing", "central_moments",
     "centroid", "feature_report", "normalize_scale", "shape_features", "InconsistencyError", "Moments2D", "MomentTensor3", "OpCounters",
     "Orientation", "ProjectionImage", "ProjectionSet", "Volume", "count_ops", "delta",
-    "VolumeMeta", "brute_force_2d", "dpm_generic_moments", "dpm_moments", "dpm_moments_batch", "harness", "run_bench", "synth", "verify_engines", "dpm_moments_file", "drt2d",
+    "VolumeMeta", "brute_force_2d", "dpm_generic_moments", "factored_moments", "naive_moments", "dpm_moments", "dpm_moments_batch", "harness", "run_bench", "synth", "verify_engines", "dpm_moments_file", "drt2d",
     "ellipsoid", "image_moments", "load_nrrd", "load_raw", "meta_from_header_file", "open_nrrd", "open_raw",
     "moment_indices", "project", "project_all",
     "project_extended", "project_subset", "random", "shift_origin", "uniform", "write_pgm", "write_raw",

@@ -30,8 +30,9 @@ EXPORTS = (
     "dpm_synth_noise_u16", "dpm_last_launch_count", "dpm_strerror", "dpm_image_moments2d",
     "dpm_project_generic", "dpm_profile_layout", "dpm_project_profile", "dpm_moments2d_profile",
     "dpm_partial_workspace_bytes", "dpm_moments_partial", "dpm_moments2d_profile_derive",
-    "dpm_moments_acc_kind", "dpm_moments_image_layout",
+    "dpm_moments_acc_kind", "dpm_moments_image_layout", "dpm_direct_workspace_bytes", "dpm_direct_moments",
 )
+DPM_DIRECT_NAIVE, DPM_DIRECT_FACTORED = 0, 1
 
 
 class VolumeDesc(ctypes.Structure):
@@ -67,6 +68,8 @@ def lib() -> ctypes.CDLL:
         "dpm_image_layout": (ctypes.c_int, [pdesc, ctypes.c_int] + [ctypes.POINTER(i64)] * 4),
         "dpm_moments_image_layout": (ctypes.c_int, [pdesc, ctypes.c_int, ctypes.c_int] + [ctypes.POINTER(i64)] * 4),
         "dpm_moments_acc_kind": (ctypes.c_int, [pdesc, ctypes.c_int]),
+        "dpm_direct_workspace_bytes": (sz, [pdesc, ctypes.c_int]),
+        "dpm_direct_moments": (ctypes.c_int, [pdesc, vp, ctypes.c_int, ctypes.c_int, vp, sz, vp, vp, vp]),
         "dpm_project_workspace_bytes": (sz, [pdesc, ctypes.c_int]),
         "dpm_project": (ctypes.c_int, [pdesc, vp, ctypes.c_int, ctypes.POINTER(vp), vp, sz, vp]),
         "dpm_project_generic": (ctypes.c_int, [pdesc, vp, ctypes.c_int, ctypes.POINTER(vp), vp]),

@@ -34,6 +34,8 @@ int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_
 int launch_derive3d(const uint64_t* acc, int64_t B, int n_img, int order, int kind, int64_t* out_i128,
                     double* out_f64, int32_t* status, cudaStream_t st);
 int launch_synth_noise(uint16_t* out, int64_t L, int64_t M, int64_t z0, int64_t nz, uint64_t seed, cudaStream_t st);
+int launch_direct3d(const dpm_volume_desc* d, const void* vox, int order, bool naive, uint64_t* planes,
+                    int64_t* out_i128, double* out_f64, cudaStream_t st);
 
 static int check_desc(const dpm_volume_desc* d) {
   if (!d) return DPM_EINVAL;
@@ -555,6 +557,23 @@ int dpm_moments_image_layout(const dpm_volume_desc* desc, int order, int img, in
   if (ai) *ai = g.ai;
   if (aj) *aj = g.aj;
   return DPM_OK;
+}
+
+size_t dpm_direct_workspace_bytes(const dpm_volume_desc* desc, int order) {
+  if (check_desc(desc) || check_order(order)) return 0;
+  return align256((size_t)(desc->B * desc->N * n2d(order) * 4) * sizeof(uint64_t));
+}
+
+int dpm_direct_moments(const dpm_volume_desc* desc, const void* d_voxels, int order, int method, void* d_ws,
+                       size_t ws_bytes, int64_t* d_m3d_i128, double* d_m3d_f64, void* stream) {
+  reset_launches();
+  int rc = check_desc(desc);
+  if (rc) return rc;
+  if (check_order(order) || !d_voxels || !d_m3d_i128 || (method != DPM_DIRECT_NAIVE && method != DPM_DIRECT_FACTORED))
+    return DPM_EINVAL;
+  if (!d_ws || ws_bytes < dpm_direct_workspace_bytes(desc, order)) return DPM_EWORKSPACE;
+  return launch_direct3d(desc, d_voxels, order, method == DPM_DIRECT_NAIVE, static_cast<uint64_t*>(d_ws),
+                         d_m3d_i128, d_m3d_f64, static_cast<cudaStream_t>(stream));
 }
 
 int dpm_last_launch_count(void) { return g_launches; }

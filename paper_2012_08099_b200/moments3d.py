@@ -99,7 +99,7 @@ def dpm_moments(volume: Volume, order: int, counters: OpCounters | None = None,
     if check_consistency:
         raise_status(st)
     vals = engine.i128_to_ints(res.i128[0].cpu().numpy())
-    dims = volume.dims if isinstance(volume, Volume) else tuple(reversed(vox.shape[-3:]))
+    dims = tuple(volume.dims) if hasattr(volume, "dims") else tuple(reversed(vox.shape[-3:]))
     _count(counters, order, dims)
     return MomentTensor3(order, dict(zip(moment_indices(order), vals)))
 
@@ -182,7 +182,7 @@ def dpm_generic_moments(volume: Volume, order: int, counters: OpCounters | None 
 
     engine.check_order(order)
     vox = _to_device(volume)
-    dims = volume.dims if isinstance(volume, Volume) else tuple(reversed(vox.shape[-3:]))
+    dims = tuple(volume.dims) if hasattr(volume, "dims") else tuple(reversed(vox.shape[-3:]))
     engine.check_envelope(dims[0], dims[1], dims[2], nat.DPM_U8 if vox.dtype == torch.uint8 else nat.DPM_U16,
                           order)
     imgs = engine.project(vox, engine.num_images(order), kernel="generic")
@@ -197,7 +197,67 @@ def dpm_generic_moments(volume: Volume, order: int, counters: OpCounters | None 
     return MomentTensor3(order, dict(zip(moment_indices(order), vals)))
 
 
+def _direct(volume: Volume, order: int, method: int, name: str, check_consistency: bool = True) -> MomentTensor3:
+    """Exact Eq. 2 sums on the device (csrc/direct3d.cu, dpm_direct_moments)."""
+    import ctypes
+
+    import torch
+
+    from . import engine
+    from .projection import _to_device
+
+    engine.check_order(order)
+    vox = _to_device(volume)
+    desc = engine.make_desc(vox)
+    dims = tuple(volume.dims) if hasattr(volume, "dims") else tuple(reversed(vox.shape[-3:]))
+    engine.check_envelope(dims[0], dims[1], dims[2], desc.dtype, order)
+    lib = nat.lib()
+    wsb = int(lib.dpm_direct_workspace_bytes(ctypes.byref(desc), order))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=vox.device)
+    n3 = len(moment_indices(order))
+    out = torch.empty((desc.B, n3, 2), dtype=torch.int64, device=vox.device)
+    nat.check(lib.dpm_direct_moments(ctypes.byref(desc), vox.data_ptr(), order, method, ws.data_ptr(), wsb,
+                                     out.data_ptr(), None, engine.stream_handle()), name)
+    torch.cuda.current_stream().synchronize()
+    vals = engine.i128_to_ints(out[0].cpu().numpy())
+    return MomentTensor3(order, dict(zip(moment_indices(order), vals)))
+
+
+def naive_moments(volume: Volume, order: int, counters: OpCounters | None = None,
+                  check_consistency: bool = True) -> MomentTensor3:
+    """Direct evaluation M[p][q][r] = sum V x^p y^q z^r (moments3d.py:78-139),
+    exact, on the device: every voxel is multiplied by every in-plane monomial
+    x^p y^q (csrc/direct3d.cu, NAIVE), the plane totals by z^r.  Counters are
+    the reference's tallies for this method: per moment, one multiply and one
+    add per voxel and per plane."""
+    res = _direct(volume, order, nat.DPM_DIRECT_NAIVE, "naive_moments")
+    if counters is not None:
+        l, m, n = volume.dims
+        k = len(moment_indices(order))
+        counters.multiplications += k * (l * m * n + n)
+        counters.additions += k * (l * m * n + n)
+    return res
+
+
+def factored_moments(volume: Volume, order: int, counters: OpCounters | None = None,
+                     check_consistency: bool = True) -> MomentTensor3:
+    """Row -> slice -> volume factored evaluation (moments3d.py:142-198),
+    exact, on the device: per x-row the K + 1 sums V x^p, rows weighted by
+    y^q per slice, slices by z^r (csrc/direct3d.cu, FACTORED).  Counters are
+    the reference's tallies for this method."""
+    res = _direct(volume, order, nat.DPM_DIRECT_FACTORED, "factored_moments")
+    if counters is not None:
+        l, m, n = volume.dims
+        pq = (order + 1) * (order + 2) // 2
+        k = len(moment_indices(order))
+        counters.multiplications += order * l * m * n + pq * m * n + k * n
+        counters.additions += (order + 1) * l * m * n + pq * m * n + k * n
+    return res
+
+
 ENGINES = {
+    "naive": naive_moments,
+    "factored": factored_moments,
     "dpm": dpm_moments,
     "dpm_generic": dpm_generic_moments,
 }

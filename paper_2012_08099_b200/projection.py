@@ -173,10 +173,19 @@ def _uploader():
         return up
 
 
+def _is_volume(volume) -> bool:
+    """This package's Volume, or any object with the reference Volume's shape
+    (a numpy ``voxels`` [z, y, x] array and ``dims``), e.g. a reference
+    ``volmoments.Volume`` handed to the engine registered in the reference's
+    ENGINES."""
+    return isinstance(volume, Volume) or (isinstance(getattr(volume, "voxels", None), np.ndarray)
+                                          and hasattr(volume, "dims"))
+
+
 def _to_device(volume):
     import torch
 
-    if isinstance(volume, Volume):
+    if _is_volume(volume):
         arr = np.ascontiguousarray(volume.voxels)
         if arr.nbytes >= (32 << 20) and arr.ndim == 3:
             dev = _uploader().upload(arr)

@@ -150,7 +150,9 @@ def test_gpu_cli_verify_and_project(tmp_path, capsys):
 
 @pytest.mark.gpu
 def test_gpu_run_bench_rows():
-    rep = harness.run_bench(max_size_mb=2, orders=(3, 6), repetitions=2)
+    rep = harness.run_bench(max_size_mb=2, orders=(3, 6), repetitions=2, engines=("dpm",))
     assert [(r.size_mb, r.order) for r in rep.rows] == [(1, 3), (1, 6), (2, 3), (2, 6)]
+    three = harness.run_bench(max_size_mb=1, orders=(3,), repetitions=1)     # default: the reference's three engines
+    assert sorted(r.engine for r in three.rows) == ["dpm", "factored", "naive"]
     for r in rep.rows:
         assert r.best_ms > 0 and r.device_ms > 0 and r.gvoxel_per_s > 0 and r.additions > 0

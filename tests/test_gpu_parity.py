@@ -12,7 +12,7 @@ import pyoracle
 import paper_2012_08099_b200 as vm
 from golden_data import (ORIENTATIONS, configs, moments, parse_moments, projections, sha,
                          volume_for)
-from paper_2012_08099_b200 import configs as synth, engine
+from paper_2012_08099_b200 import _native as nat, configs as synth, engine
 from paper_2012_08099_b200.errors import InconsistencyError
 
 pytestmark = pytest.mark.gpu
@@ -250,3 +250,43 @@ def test_image_moments_2d_errors(cuda):
         vm.image_moments(np.ones((3, 3)), 7)
     with pytest.raises(OverflowError):
         vm.image_moments(np.full((4000, 4000), 2**32 - 1, dtype=np.uint64), 6)
+
+
+@pytest.mark.parametrize("order", [3, 4, 5, 6])
+@pytest.mark.parametrize("shape,dt", [((9, 7, 5), np.uint8), ((13, 11, 203), np.uint16), ((5, 300, 4), np.uint16),
+                                      ((20, 16, 264), np.int16)])
+def test_direct_engines_naive_and_factored(cuda, order, shape, dt):
+    """The reference's direct engines on the device (csrc/direct3d.cu): exact
+    like the oracle's direct sum, for every dtype and shape, batch included."""
+    rng = np.random.default_rng(order + sum(shape))
+    if dt == np.int16:
+        vol = rng.integers(-1024, 3072, size=shape).astype(np.int16)
+        want = oracle.naive((vol.astype(np.int32) + 1024).astype(np.uint16), order)
+        for method in (0, 1):
+            import ctypes
+            v = torch.from_numpy(vol).cuda()
+            d = engine.make_desc(v, 1024)
+            wsb = int(nat.lib().dpm_direct_workspace_bytes(ctypes.byref(d), order))
+            ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+            out = torch.empty((1, len(want), 2), dtype=torch.int64, device="cuda")
+            assert nat.lib().dpm_direct_moments(ctypes.byref(d), v.data_ptr(), order, method, ws.data_ptr(), wsb,
+                                                out.data_ptr(), None, None) == 0
+            torch.cuda.synchronize()
+            assert engine.i128_to_ints(out[0].cpu().numpy()) == [want[k] for k in vm.moment_indices(order)]
+        return
+    vol = rng.integers(0, np.iinfo(dt).max + 1, size=shape).astype(dt)
+    v = vm.Volume(vol)
+    want = oracle.naive(vol, order)
+    assert vm.naive_moments(v, order).values == want
+    assert vm.factored_moments(v, order).values == want
+    assert vm.dpm_moments(v, order).values == want
+
+
+def test_direct_engines_full_width_exact(cuda):
+    """2048-wide 16-bit volumes at order 4, where the reference's naive and
+    factored engines raise OverflowError (moments3d.py:121-127, 158-161): exact
+    here, equal to the projection engine."""
+    vol = engine.synth_noise(2048, 64, 0, 8, 5).cpu().numpy()
+    v = vm.Volume(vol)
+    d = vm.dpm_moments(v, 4).values
+    assert vm.naive_moments(v, 4).values == d and vm.factored_moments(v, 4).values == d

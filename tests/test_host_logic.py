@@ -128,3 +128,20 @@ def test_int16_offset_range_is_validated():
         engine.make_desc(torch.zeros((2, 2, 2), dtype=torch.uint16), offset=5)
     with pytest.raises(ValueError):
         engine.make_desc(ok, offset=200000)
+
+
+def test_volmoments_dropin_surface():
+    """``import volmoments`` resolves to this package: the reference's module
+    names alias the engine's modules, the public names exist, and the only
+    reference exports missing are the documented integral-route internals."""
+    import volmoments
+    import volmoments.moments3d
+    import volmoments.projection
+    from oracle import reference
+    assert volmoments.moments3d is vm.moments3d and volmoments.projection is vm.projection
+    assert volmoments.dpm_moments is vm.dpm_moments
+    assert set(volmoments.moments3d.ENGINES) == {"naive", "factored", "dpm", "dpm_generic"}
+    ref = reference.load()
+    if ref is not None:
+        missing = set(ref.__all__) - set(dir(volmoments))
+        assert missing <= {"IntegralSet", "integrals", "moments_1d", "assemble_2d"}, missing
