@@ -90,19 +90,24 @@ template <int AS> struct Ring {
   static constexpr int WORDS = 8 * RP;
   // slot index of block b: lanes' blocks n + AS l map to consecutive slots
   static __device__ __forceinline__ int idx(int b) {
-    const int m = b % R;
-    return (m % AS) * 32 + m / AS;
+    const uint32_t m = (uint32_t)b % (uint32_t)R;
+    return (int)((m % AS) * 32 + m / AS);
   }
 };
 // CTA profile ring: live span 31 AS + 1 plus the warps' drift (< STAGES steps)
-// plus the flush lag (a block is flushed STAGES steps after it completes)
+// plus the flush lag (a block is flushed STAGES steps after it completes).
+// R is a power of two (a multiple of 32): for odd AS the lanes' blocks n + AS l
+// are 32 distinct banks as they are; for AS = 2 the two parity classes are
+// split into halves (slot (m & 1) R/2 + m/2), so no division by AS at all
+__host__ __device__ constexpr int zs_pow2_at_least(int v) { int r = 32; while (r < v) r *= 2; return r; }
 template <int AS, int STAGES> struct PRing {
-  static constexpr int R = ((32 * AS + 2 * STAGES + 2 + AS - 1) / AS) * AS;
+  static constexpr int R = zs_pow2_at_least(32 * AS + 2 * STAGES + 2);
   static constexpr int RP = R + 1;
   static constexpr int WORDS = 8 * RP;
   static __device__ __forceinline__ int idx(int b) {
-    const int m = b % R;
-    return (m % AS) * (R / AS) + m / AS;
+    const uint32_t m = (uint32_t)b & (uint32_t)(R - 1);
+    if constexpr (AS % 2 == 1) return (int)m;
+    else return (int)((m & 1u) * (R / 2) + (m >> 1));
   }
 };
 
@@ -116,7 +121,7 @@ template <typename T, int K, int NW, int VX, int STAGES> struct ZGeo {
   static constexpr int WARP_RING = ring_off(NOB);               // words per warp
   static constexpr int PR_WORDS = PRing<ASP, STAGES>::WORDS;
   static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + (size_t)NW * WARP_RING * 4 + PR_WORDS * 4 + 8 +
-                                 2 * STAGES * 8 + 128 + 64 * NW;   // + the producer state and the warps' cursors
+                                 2 * STAGES * 8 + 128 + 64 * NW + 96 * STAGES;   // + producer state, warps' cursors, stage cursors
 };
 
 // ---- lane vectors ------------------------------------------------------------
@@ -367,8 +372,28 @@ __device__ __forceinline__ void zdecode(const ZParams& p, int64_t col, int32_t& 
   b = (int32_t)(r / p.n_yg);
 }
 
+// Who refills a stage (DPM_ZS_PWARP):
+//   0: thread 0, for stage g - ZLAG, from inside its own step loop (waits on
+//      the stage's empty mbarrier);
+//   1: one extra warp that only produces (refills a stage the moment the last
+//      compute warp releases it) -- costs a register-file quarter per SMSP;
+//   2: the compute warp that releases a stage LAST refills it (per-stage release
+//      counters; every stage has its own cursor, advanced STAGES steps per use,
+//      so refills of different stages never share state).
+#ifndef DPM_ZS_PWARP
+#define DPM_ZS_PWARP 0   // measured: 1 spills (the fourth warp per SMSP caps registers at 168), 2 is 8 % slower (x25)
+#endif
+constexpr int ZPW = DPM_ZS_PWARP == 1 ? 1 : 0;
+constexpr bool ZLAST = DPM_ZS_PWARP == 2;
+
+// barrier over the NW compute warps only (the producer warp never joins it)
+template <int NW> __device__ __forceinline__ void zs_sync() {
+  if constexpr (ZPW) asm volatile("bar.sync 1, %0;" ::"n"(32 * NW) : "memory");
+  else __syncthreads();
+}
+
 template <typename T, int K, int NW, int VX, int STAGES, int FMAMASK>
-__global__ void __launch_bounds__(32 * NW, 1) zstream_kernel(const __grid_constant__ CUtensorMap tmap, const ZParams p) {
+__global__ void __launch_bounds__(32 * (NW + ZPW), 1) zstream_kernel(const __grid_constant__ CUtensorMap tmap, const ZParams p) {
   using G = ZGeo<T, K, NW, VX, STAGES>;
   using V = typename ZVec<T, VX>::type;
   constexpr int NOB = G::NOB, SX = G::SX;
@@ -392,9 +417,12 @@ __global__ void __launch_bounds__(32 * NW, 1) zstream_kernel(const __grid_consta
   uint64_t* empty = full + STAGES;
   ZProd* prod = reinterpret_cast<ZProd*>(empty + STAGES);   // producer state (thread 0 only)
   ZSeg* segs = reinterpret_cast<ZSeg*>(prod + 1);            // [NW] each warp's segment cursor
+  ZProd* prods = reinterpret_cast<ZProd*>(segs + NW);        // [STAGES] per-stage cursors (ZLAST)
+  uint32_t* rel = reinterpret_cast<uint32_t*>(prods + STAGES);   // [STAGES] release counters (ZLAST)
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 
-  for (int i = tid; i < NW * G::WARP_RING + G::PR_WORDS; i += 32 * NW) rings[i] = 0;
+  if (w < NW)
+    for (int i = tid; i < NW * G::WARP_RING + G::PR_WORDS; i += 32 * NW) rings[i] = 0;
   auto issue = [&]() {   // thread 0: the next step of the sequence into its stage
     ZProd st = *prod;
     if (st.seg.done) return;
@@ -409,6 +437,24 @@ __global__ void __launch_bounds__(32 * NW, 1) zstream_kernel(const __grid_consta
     }
     *prod = st;
   };
+  auto advance1 = [&](ZProd& st) {
+    if (st.seg.done) return;
+    if (++st.n == st.seg.n1) {
+      st.seg.next(p);
+      if (!st.seg.done) { st.n = st.seg.n0; zdecode(p, st.seg.col, st.xt, st.yg, st.b); }
+    }
+  };
+  // ZLAST: stage k's cursor -> TMA into stage k, then advance it STAGES steps
+  auto issue_stage = [&](int k) {
+    ZProd st = prods[k];
+    if (st.seg.done) return;
+    ptx::mbar_arrive_expect_tx(&full[k], G::STAGE_BYTES);
+    ptx::tma_load_4d_hint(stages + (size_t)k * G::STAGE_BYTES, &tmap, &full[k], st.xt * SX, st.yg * NW, st.n * 8,
+                          st.b, ptx::policy_evict_first());
+    #pragma unroll 1
+    for (int i = 0; i < STAGES; ++i) advance1(st);
+    prods[k] = st;
+  };
   if (tid == 0) {
     ptx::prefetch_tmap(&tmap);
     for (int i = 0; i < STAGES; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&empty[i], NW); }
@@ -417,11 +463,30 @@ __global__ void __launch_bounds__(32 * NW, 1) zstream_kernel(const __grid_consta
     st.k = 0;
     st.seg.first(p);
     if (!st.seg.done) { st.n = st.seg.n0; zdecode(p, st.seg.col, st.xt, st.yg, st.b); }
-    *prod = st;
-    for (int h = 0; h < STAGES; ++h) issue();
+    if constexpr (ZLAST) {
+      for (int h = 0; h < STAGES; ++h) { prods[h] = st; rel[h] = 0; advance1(st); }
+      for (int h = 0; h < STAGES; ++h) issue_stage(h);
+    } else {
+      *prod = st;
+      for (int h = 0; h < STAGES; ++h) issue();
+    }
   }
-  if (lane == 0) segs[w].first(p);
+  if (lane == 0 && w < NW) segs[w].first(p);
   __syncthreads();
+  if constexpr (ZPW) {
+    if (w == NW) {   // producer warp: refill each stage as soon as every compute warp released it
+      if (lane == 0) {
+        int kk = 0;
+        uint32_t ph = 0;
+        while (!prod->seg.done) {
+          ptx::mbar_wait_addr(ptx::smem_addr(empty) + 8u * (uint32_t)kk, ph);
+          issue();
+          if (++kk == STAGES) { kk = 0; ph ^= 1u; }
+        }
+      }
+      return;
+    }
+  }
 
   const uint32_t bar_a = ptx::smem_addr(full);               // full[k] at +8k, empty[k] at +8(STAGES + k)
   const uint32_t wring_a = ptx::smem_addr(rings + w * G::WARP_RING);
@@ -435,7 +500,11 @@ __global__ void __launch_bounds__(32 * NW, 1) zstream_kernel(const __grid_consta
 
   // step counter (all warps): step g in stage k / phase ph; step g - ZLAG in stage kl /
   // phase phl; warp pw flushes the profile block of step g
-  constexpr int ZLAG = STAGES >= 4 ? 2 : 1;
+#ifndef DPM_ZS_ZLAG
+#define DPM_ZS_ZLAG (K >= 6 ? 2 : 1)   // measured best per order (x26)
+#endif
+  constexpr int ZLAG = STAGES >= 4 ? DPM_ZS_ZLAG : 1;
+  static_assert(sizeof(ZProd) <= 96, "stage cursor budget (ZGeo::SMEM)");
   int k = 0, pw = 0, kl = 0, lagc = 0;
   uint32_t ph = 0, phl = 0;
   while (true) {
@@ -480,7 +549,7 @@ __global__ void __launch_bounds__(32 * NW, 1) zstream_kernel(const __grid_consta
 
     // one step (8 planes) at window phase R = rn mod ZU
     auto step = [&]<int R>(const int rn) {
-      if (tid == 0 && lagc >= ZLAG) {
+      if (!ZPW && !ZLAST && tid == 0 && lagc >= ZLAG) {
         // producer: once every warp released step g - ZLAG, refill its stage with
         // step g - ZLAG + STAGES.  The lag leaves the other warps ZLAG - 1 steps of
         // slack before the producer has to wait for the slowest of them.
@@ -549,7 +618,15 @@ __global__ void __launch_bounds__(32 * NW, 1) zstream_kernel(const __grid_consta
         ptx::red_global_add_if(frow + i, v, v != 0 && frow != nullptr && i >= 0 && i < fW);
       }
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_addr(bar_a + 8u * (uint32_t)(STAGES + k));
+      if (lane == 0) {
+        if constexpr (ZLAST) {   // the last of the NW warps to release stage k refills it
+          uint32_t old;
+          asm volatile("atom.shared.inc.u32 %0, [%1], %2;" : "=r"(old) : "r"(ptx::smem_addr(rel + k)), "r"((uint32_t)(NW - 1)) : "memory");
+          if (old == (uint32_t)(NW - 1)) issue_stage(k);
+        } else {
+          ptx::mbar_arrive_addr(bar_a + 8u * (uint32_t)(STAGES + k));
+        }
+      }
       if (++k == STAGES) { k = 0; ph ^= 1u; }
       if (lagc < ZLAG) ++lagc;
       else if (++kl == STAGES) { kl = 0; phl ^= 1u; }
@@ -614,7 +691,7 @@ __global__ void __launch_bounds__(32 * NW, 1) zstream_kernel(const __grid_consta
     for (int kk = 0; kk < VX; ++kk)
       if (cs[kk] != 0 && yok && xl + kk < p.L) atomicAdd(p.img[DPM_IMG_YZ] + (b * p.L + xl + kk) * p.M + y, cs[kk]);
     // CTA profile ring: every warp has emitted all of the segment; flush what is left
-    __syncthreads();
+    zs_sync<NW>();
     {
       const int first = rn_end >= STAGES ? rn_end - STAGES : 0;   // blocks the step loop did not flush
       const int nblk = rn_end + 32 * ASP - first;
@@ -628,7 +705,7 @@ __global__ void __launch_bounds__(32 * NW, 1) zstream_kernel(const __grid_consta
       }
     }
     if (lane == 0) segs[w].next(p);
-    __syncthreads();
+    zs_sync<NW>();
   }
 }
 
@@ -721,7 +798,7 @@ static int launch_zs(const dpm_volume_desc* d, const void* vox, const ImageSet& 
   if (ensure_smem(zstream_kernel<T, K, NW, VX, S, C::FMAMASK>, G::SMEM, attr_mask)) return DPM_ECUDA;
   const int64_t units = p.run_mode ? p.ncol * p.ns : p.ncol * p.zsplit;
   const int grid = (int)imin64(G_, units);
-  zstream_kernel<T, K, NW, VX, S, C::FMAMASK><<<grid, 32 * NW, G::SMEM, st>>>(map, p);
+  zstream_kernel<T, K, NW, VX, S, C::FMAMASK><<<grid, 32 * (NW + ZPW), G::SMEM, st>>>(map, p);
   return DPM_OK;
 }
 

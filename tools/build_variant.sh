@@ -9,7 +9,7 @@ B=$ROOT/tools/ab/build_$NAME
 rm -rf "$B"; mkdir -p "$B"
 for f in "$SRC"/*.cu; do
   nvcc $FLAGS -std=c++20 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC \
-    -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr -c "$f" -o "$B/$(basename "${f%.cu}").o" &
+    -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr -c "$f" -o "$B/$(basename "${f%.cu}").o" 2>/dev/null &
 done
 wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$ROOT/tools/ab/lib_$NAME.so" "$B"/*.o -lcudart_static -Xcompiler -fvisibility=hidden
