@@ -21,6 +21,9 @@ int launch_project_generic(const dpm_volume_desc* d, const void* vox, const Imag
 int launch_project_zstream(const dpm_volume_desc* d, const void* vox, int order, const ImageSet& s,
                            unsigned long long* prof, int64_t WQ, cudaStream_t st, bool* handled);
 bool zstream_eligible(const dpm_volume_desc* d, const void* vox);
+bool fused_batch_eligible(const dpm_volume_desc* d, const void* vox, int order);
+int launch_fused_batch(const dpm_volume_desc* d, const void* vox, int order, uint64_t* acc, unsigned int* cnt,
+                       int64_t* out_i128, double* out_f64, int32_t* status, cudaStream_t st, bool* handled);
 int launch_project_stream(const dpm_volume_desc* d, const void* vox, const ImageSet& s, unsigned long long* prof,
                           cudaStream_t st, bool* handled);
 int profile_shift(int n_img);
@@ -529,6 +532,16 @@ int dpm_moments(const dpm_volume_desc* desc, const void* d_voxels, int order, vo
   f.i128 = d_m3d_i128;
   f.f64 = d_m3d_f64;
   f.status = d_status;
+  if (fused_batch_eligible(desc, d_voxels, order)) {
+    // small uint8 volumes (<= 128 wide and deep, order 3): one memset of
+    // [counters | acc] and ONE launch for projection, moments and epilogue
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(f.cnt, 0, cbytes + acc_bytes_of(desc, order), st) != cudaSuccess) return DPM_ECUDA;
+    reset_launches();
+    bool handled = false;
+    rc = launch_fused_batch(desc, d_voxels, order, acc, f.cnt, d_m3d_i128, d_m3d_f64, d_status, st, &handled);
+    if (rc || handled) return rc;
+  }
   // memset, projection pass, one moments launch that ends with the epilogue
   return moments_partial_impl(desc, d_voxels, order, pws, pbytes, acc, stream, true, &f);
 }
