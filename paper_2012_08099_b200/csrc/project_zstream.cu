@@ -58,6 +58,10 @@
 #include "dpm_common.cuh"
 #include "ptx.cuh"
 
+#ifndef DPM_ZS_XY_IDP
+#define DPM_ZS_XY_IDP 1   // XY-slot plane sums by IDP dot products on the FMA pipe (x30: cfg5 -1 %)
+#endif
+#include <type_traits>
 #ifndef DPM_ZS_GP
 #define DPM_ZS_GP 4   // planes per fold group when a |s| >= 2 form is folded on the ALU pipe
 #endif
@@ -573,17 +577,27 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), 1) zstream_kernel(const __gri
       #pragma unroll
       for (int h = 0; h < 8 / GP; ++h) {
         uint32_t P[GP][VX];
+        V draw[GP];
         #pragma unroll
         for (int gg = 0; gg < GP; ++gg) {
           const int t = GP * h + gg;
           const V d = ptx::lds_vec<V>(tile_a + (uint32_t)(t * NW * SX * (int)sizeof(T)));
+          draw[gg] = d;
           ZUnpack<T>::run(d, P[gg], z + t < p.N ? off_lane : 0, p.one << 16);
         }
         // XY slot: plane sums over the lane's x, one warp redux per plane
         #pragma unroll
         for (int gg = 0; gg < GP; ++gg) {
           uint32_t sm = 0;
-          if constexpr (VX == 8) sm = (P[gg][0] + P[gg][1] + P[gg][2]) + (P[gg][3] + P[gg][4]) + (P[gg][5] + P[gg][6]) + P[gg][7];
+          if constexpr (DPM_ZS_XY_IDP && !std::is_same_v<T, int16_t>) {
+            // byte / halfword dot products with ones on the FMA pipe, straight
+            // from the packed words (the ALU pipe carries the folds)
+            const uint32_t* wd = reinterpret_cast<const uint32_t*>(&draw[gg]);
+            if constexpr (sizeof(T) == 2) sm = __dp2a_lo(wd[0], 0x0101u, __dp2a_lo(wd[1], 0x0101u, __dp2a_lo(wd[2], 0x0101u, __dp2a_lo(wd[3], 0x0101u, 0u))));
+            else sm = __dp4a(wd[0], 0x01010101u, __dp4a(wd[1], 0x01010101u, 0u));
+          } else if constexpr (VX == 8) {
+            sm = (P[gg][0] + P[gg][1] + P[gg][2]) + (P[gg][3] + P[gg][4]) + (P[gg][5] + P[gg][6]) + P[gg][7];
+          }
           const uint32_t r = __reduce_add_sync(0xffffffffu, sm);
           yzmine = lane == GP * h + gg ? r : yzmine;
         }
