@@ -8,6 +8,20 @@ namespace dpm {
 
 typedef __int128 i128;
 
+// DPM_DERIVE_PROBE (development builds only, tools/microbench/derive_probe.cu):
+// %globaltimer stamps at the epilogue's phase boundaries, per warp
+#ifdef DPM_DERIVE_PROBE
+__device__ unsigned long long g_derive_probe[64][8];
+__device__ __forceinline__ void derive_probe(int w, int i) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if ((threadIdx.x & 31) == 0 && w < 64) g_derive_probe[w][i] = t;
+}
+#define DPM_PROBE(i) derive_probe(w, i)
+#else
+#define DPM_PROBE(i) ((void)0)
+#endif
+
 __device__ __forceinline__ i128 acc_to_i128(const uint64_t* a) {
   unsigned __int128 v = (unsigned __int128)a[0];
   v += ((unsigned __int128)a[1]) << 32;
@@ -86,9 +100,11 @@ __device__ void derive_volume(const uint64_t* a, int64_t b, int n_img, int kind,
   int32_t& sst = *sst_p;
   const int nthreads = blockDim.x, nwarps = nthreads >> 5;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  DPM_PROBE(0);
   for (int i = tid; i < n_img * N2 * 4; i += nthreads) sa[i] = coherent ? __ldcg(a + i) : a[i];
   if (tid == 0) sst = 0;
   __syncthreads();
+  DPM_PROBE(1);
   int32_t st = 0;
   auto m2 = [&](int img, int p, int q) -> i128 { return acc_to_i128(sa + (img * N2 + idx2(K, p, q)) * 4); };
   auto put = [&](int p, int q, int r, i128 v) {
@@ -101,36 +117,44 @@ __device__ void derive_volume(const uint64_t* a, int64_t b, int n_img, int kind,
   if (tid > 0 && tid < n_img && m2(tid, 0, 0) != m2(0, 0, 0)) st |= DPM_ST_MASS;
 
   // placement: XY -> (p,q,0), YZ -> (0,p,q), ZX -> (q,0,p); first route wins, others must agree
-  {
-    int n = 0;
-    for (int p = 0; p <= K; ++p)
-      for (int q = 0; q <= K - p; ++q)
-        for (int r = 0; r <= K - p - q; ++r, ++n) {
-          if (n % nthreads != tid || (p > 0 && r > 0 && (q > 0 || prof))) continue;
-          bool have = false;
-          i128 v = 0;
-          auto route = [&](i128 x) {
-            if (!have) { have = true; v = x; }
-            else if (x != v) st |= DPM_ST_DISAGREE;
-          };
-          if (r == 0) route(m2(DPM_IMG_XY, p, q));
-          if (p == 0) route(m2(DPM_IMG_YZ, q, r));
-          if (q == 0 && !prof) route(m2(DPM_IMG_ZX, r, p));
-          put(p, q, r, v);
-        }
+  // (one moment per thread: n3d <= 84 <= blockDim; the index is decoded, not
+  // searched with a run-time modulo per candidate -- that loop was most of the
+  // epilogue's latency)
+  // (counted from the LAST thread: warp 0 takes the costliest solve group below)
+  for (int n = nthreads - 1 - tid; n < N3; n += nthreads) {
+    int p = 0, rem = n;
+    while (rem >= (K - p + 1) * (K - p + 2) / 2) { rem -= (K - p + 1) * (K - p + 2) / 2; ++p; }
+    int q = 0;
+    while (rem >= K - p - q + 1) { rem -= K - p - q + 1; ++q; }
+    const int r = rem;
+    if (p > 0 && r > 0 && (q > 0 || prof)) continue;
+    bool have = false;
+    i128 v = 0;
+    auto route = [&](i128 x) {
+      if (!have) { have = true; v = x; }
+      else if (x != v) st |= DPM_ST_DISAGREE;
+    };
+    if (r == 0) route(m2(DPM_IMG_XY, p, q));
+    if (p == 0) route(m2(DPM_IMG_YZ, q, r));
+    if (q == 0 && !prof) route(m2(DPM_IMG_ZX, r, p));
+    put(p, q, r, v);
   }
 
+  DPM_PROBE(2);
   // cross-axis groups (q, a = p + r): unknowns u_c = C(a,c) M_{a-c,q,c}, c = 1..a-1, from
   //   f_t = M^t_{a,q} - M_{a,q,0} - t^a M_{0,q,a} = sum_c t^c u_c
   // over the oblique images t = 1, -1, 2, -2 (and, for q = 0 in profile mode,
   // the profile as the next t).  Groups with a = 1 only check.
-  if (lane == 0) {
+  // Group (q, p) runs on lane q of warp (K - p) mod nwarps: the lanes of a warp
+  // share p, so they share the solve path (n = p - 1 unknowns) and run the
+  // groups of a p side by side (one lane each) instead of one after another;
+  // the costliest p (the most unknowns) get warps of their own first.
+  {
     const int tv[5] = {1, -1, 2, -2, 3};
     const int n_obl = n_img - 3;
-    int g = 0;
-    for (int q = prof ? 0 : 1; q <= K - 1; ++q)
-      for (int p = 1; p <= K - q; ++p, ++g) {
-        if (g % nwarps != w) continue;
+    const int q = lane;
+    for (int p = K - w; p >= 1; p -= nwarps) {
+        if (q < (prof ? 0 : 1) || q > K - p) continue;
         const int n = p - 1;                               // unknowns
         const int avail = (q == 0) ? n_obl + 1 : n_obl;    // equations (q = 0 only in profile mode)
         const i128 mxy = m2(DPM_IMG_XY, p, q), myz = m2(DPM_IMG_YZ, q, p);
@@ -194,9 +218,11 @@ __device__ void derive_volume(const uint64_t* a, int64_t b, int n_img, int kind,
         if (!ok) st |= DPM_ST_NONEXACT;
       }
   }
+  DPM_PROBE(3);
   st = __reduce_or_sync(0xffffffffu, (unsigned)st);
   if (lane == 0 && st) atomicOr(&sst, st);
   __syncthreads();
+  DPM_PROBE(4);
   if (tid == 0) status[b] = sst;
 }
 
