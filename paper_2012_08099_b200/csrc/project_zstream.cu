@@ -58,6 +58,18 @@
 #include "dpm_common.cuh"
 #include "ptx.cuh"
 
+#ifndef DPM_ZS_HALF
+#define DPM_ZS_HALF 1   // orders 5-6: windows spanning one fold group, emitted per group, 12 warps (v33)
+#endif
+#ifndef DPM_ZS_HALF_MINK
+#define DPM_ZS_HALF_MINK 5   // lowest order that uses the group-wise windows
+#endif
+#ifndef DPM_ZS_NW34
+#define DPM_ZS_NW34 12       // warps per CTA at orders 3-4
+#endif
+#ifndef DPM_ZS_CS_FMA
+#define DPM_ZS_CS_FMA 0   // YZ-slot x sums with IMAD-by-1 (FMA pipe) instead of 3-input adds
+#endif
 #ifndef DPM_ZS_XY_IDP
 #define DPM_ZS_XY_IDP 1   // XY-slot plane sums by IDP dot products on the FMA pipe (x30: cfg5 -1 %)
 #endif
@@ -322,6 +334,34 @@ __device__ __forceinline__ void zemit_all_r(uint32_t (&win)[NB * 8], uint32_t ri
   for (int c = 0; c < NB * 8; ++c) win[c] = 0u;
 }
 
+// ---- group-wise windows (DPM_ZS_HALF) -------------------------------------------
+// The window of a form only has to span ONE fold group of GP planes: after the
+// group, its first GP cells are complete for this lane (every later plane of
+// the step lands at a higher cell), so they are emitted -- ring rows GP h ..
+// GP h + GP - 1 of the step's block -- and the window slides by GP cells.
+// GP + |s|(VX - 1) cells instead of 8 + |s|(VX - 1): the order-6 windows need
+// 83 registers instead of 103, which lets 12 warps (3 per scheduler) fit.
+template <int S, int VX, int GP> __host__ __device__ constexpr int zs_gwin() { return GP + zs_abs(S) * (VX - 1); }
+template <int GP, int NWIN, typename RingT>
+__device__ __forceinline__ void zemit_group(uint32_t (&win)[NWIN], uint32_t ring_addr, int blk, int h) {
+  const uint32_t a = ring_addr + 4u * (uint32_t)RingT::idx(blk);
+  #pragma unroll
+  for (int k = 0; k < GP; ++k) ptx::red_shared_add_dyn(a + 4u * (uint32_t)((GP * h + k) * RingT::RP), win[k]);
+  #pragma unroll
+  for (int c = 0; c < NWIN; ++c) win[c] = c + GP < NWIN ? win[c + GP] : 0u;
+}
+// segment end (after the last group's slide): cells [0, 7|s|) belong to blocks blk + c / 8
+template <int S, int VX, int NWIN, typename RingT>
+__device__ __forceinline__ void zemit_group_tail(uint32_t (&win)[NWIN], uint32_t ring_addr, int blk) {
+  #pragma unroll
+  for (int c = 0; c < zs_abs(S) * (VX - 1); ++c) {
+    const uint32_t v = win[c];
+    if (v != 0) ptx::red_shared_add_dyn(ring_addr + 4u * (uint32_t)(RingT::idx(blk + c / 8) + (c % 8) * RingT::RP), v);
+  }
+  #pragma unroll
+  for (int c = 0; c < NWIN; ++c) win[c] = 0u;
+}
+
 // Segment iterator shared by the producer and the consumers: the CTA's
 // sequence of (column, n0, n1) step ranges.
 struct ZSeg {
@@ -410,6 +450,7 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), 1) zstream_kernel(const __gri
   // for |s| = 2, (t, t+3) for |s| = 3 -- groups of 4 when a form with |s| >= 2 is
   // folded on the ALU pipe, 2 (fewer live registers) when those go to the FMA pipe
   constexpr int GP = (NOB <= 2 || (FMAMASK & 12) == 12) && ((FMAMASK & 16) || ASP == 1) ? 2 : DPM_ZS_GP;
+  constexpr bool HALF = DPM_ZS_HALF && K >= DPM_ZS_HALF_MINK;   // group-wise windows (see zemit_group)
   using PR = PRing<ASP, STAGES>;
   constexpr uint32_t R0 = G::ring_off(0) * 4, R1 = G::ring_off(1) * 4, R2 = G::ring_off(2) * 4,
                      R3 = G::ring_off(3) * 4;
@@ -537,17 +578,20 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), 1) zstream_kernel(const __gri
 
     constexpr int NB0 = zs_nb(zs_abs(S0)), NB1 = zs_nb(zs_abs(S1)), NB2 = zs_nb(zs_abs(S2)), NB3 = zs_nb(zs_abs(S3));
     constexpr int NBP = zs_nb(ASP);
-    uint32_t w0[NB0 * 8], w1[NB1 * 8], w2[NB2 * 8], w3[NB3 * 8], wq[NBP * 8], cs[VX];
+    constexpr int WS0 = HALF ? zs_gwin<S0, VX, GP>() : NB0 * 8, WS1 = HALF ? zs_gwin<S1, VX, GP>() : NB1 * 8;
+    constexpr int WS2 = HALF ? zs_gwin<S2, VX, GP>() : NB2 * 8, WS3 = HALF ? zs_gwin<S3, VX, GP>() : NB3 * 8;
+    constexpr int WSP = HALF ? zs_gwin<SP, VX, GP>() : NBP * 8;
+    uint32_t w0[WS0], w1[WS1], w2[WS2], w3[WS3], wq[WSP], cs[VX];
     #pragma unroll
-    for (int i = 0; i < NB0 * 8; ++i) w0[i] = 0;
+    for (int i = 0; i < WS0; ++i) w0[i] = 0;
     #pragma unroll
-    for (int i = 0; i < NB1 * 8; ++i) w1[i] = 0;
+    for (int i = 0; i < WS1; ++i) w1[i] = 0;
     #pragma unroll
-    for (int i = 0; i < NB2 * 8; ++i) w2[i] = 0;
+    for (int i = 0; i < WS2; ++i) w2[i] = 0;
     #pragma unroll
-    for (int i = 0; i < NB3 * 8; ++i) w3[i] = 0;
+    for (int i = 0; i < WS3; ++i) w3[i] = 0;
     #pragma unroll
-    for (int i = 0; i < NBP * 8; ++i) wq[i] = 0;
+    for (int i = 0; i < WSP; ++i) wq[i] = 0;
     #pragma unroll
     for (int i = 0; i < VX; ++i) cs[i] = 0;
 
@@ -604,21 +648,40 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), 1) zstream_kernel(const __gri
         // YZ slot: x-sums over z
         #pragma unroll
         for (int kk = 0; kk < VX; ++kk) {
-          if constexpr (GP == 4) cs[kk] = cs[kk] + (P[0][kk] + P[1][kk]) + (P[2][kk] + P[3][kk]);
+          if constexpr (DPM_ZS_CS_FMA) {
+            #pragma unroll
+            for (int gg = 0; gg < GP; ++gg) cs[kk] = ptx::mad_u32(P[gg][kk], p.one, cs[kk]);
+          } else if constexpr (GP == 4) cs[kk] = cs[kk] + (P[0][kk] + P[1][kk]) + (P[2][kk] + P[3][kk]);
           else cs[kk] = cs[kk] + P[0][kk] + P[GP - 1][kk];
         }
-        zfold_r<S0, VX, GP, (FMAMASK & 1) != 0, NB0, R % NB0>(w0, P, GP * h, p.one);
-        if constexpr (NOB > 1) zfold_r<S1, VX, GP, (FMAMASK & 2) != 0, NB1, R % NB1>(w1, P, GP * h, p.one);
-        if constexpr (NOB > 2) zfold_r<S2, VX, GP, (FMAMASK & 4) != 0, NB2, R % NB2>(w2, P, GP * h, p.one);
-        if constexpr (NOB > 3) zfold_r<S3, VX, GP, (FMAMASK & 8) != 0, NB3, R % NB3>(w3, P, GP * h, p.one);
-        zfold_r<SP, VX, GP, (FMAMASK & 16) != 0, NBP, R % NBP>(wq, P, GP * h, p.one);
+        if constexpr (HALF) {
+          // fold the group into windows spanning one group, emit its completed cells, slide
+          zfold<S0, VX, GP, (FMAMASK & 1) != 0, WS0>(w0, P, 0, p.one);
+          if constexpr (NOB > 1) zfold<S1, VX, GP, (FMAMASK & 2) != 0, WS1>(w1, P, 0, p.one);
+          if constexpr (NOB > 2) zfold<S2, VX, GP, (FMAMASK & 4) != 0, WS2>(w2, P, 0, p.one);
+          if constexpr (NOB > 3) zfold<S3, VX, GP, (FMAMASK & 8) != 0, WS3>(w3, P, 0, p.one);
+          zfold<SP, VX, GP, (FMAMASK & 16) != 0, WSP>(wq, P, 0, p.one);
+          zemit_group<GP, WS0, Ring<zs_abs(S0)>>(w0, wring_a + R0, rn + zs_abs(S0) * (S0 > 0 ? lpp : lpm), h);
+          if constexpr (NOB > 1) zemit_group<GP, WS1, Ring<zs_abs(S1)>>(w1, wring_a + R1, rn + zs_abs(S1) * (S1 > 0 ? lpp : lpm), h);
+          if constexpr (NOB > 2) zemit_group<GP, WS2, Ring<zs_abs(S2)>>(w2, wring_a + R2, rn + zs_abs(S2) * (S2 > 0 ? lpp : lpm), h);
+          if constexpr (NOB > 3) zemit_group<GP, WS3, Ring<zs_abs(S3)>>(w3, wring_a + R3, rn + zs_abs(S3) * (S3 > 0 ? lpp : lpm), h);
+          zemit_group<GP, WSP, PR>(wq, pring_a, rn + ASP * (SP > 0 ? lpp : lpm), h);
+        } else {
+          zfold_r<S0, VX, GP, (FMAMASK & 1) != 0, NB0, R % NB0>(w0, P, GP * h, p.one);
+          if constexpr (NOB > 1) zfold_r<S1, VX, GP, (FMAMASK & 2) != 0, NB1, R % NB1>(w1, P, GP * h, p.one);
+          if constexpr (NOB > 2) zfold_r<S2, VX, GP, (FMAMASK & 4) != 0, NB2, R % NB2>(w2, P, GP * h, p.one);
+          if constexpr (NOB > 3) zfold_r<S3, VX, GP, (FMAMASK & 8) != 0, NB3, R % NB3>(w3, P, GP * h, p.one);
+          zfold_r<SP, VX, GP, (FMAMASK & 16) != 0, NBP, R % NBP>(wq, P, GP * h, p.one);
+        }
       }
-      // emit the completed cells (block rn + AS l' of each form); the window slides by rotation
-      zemit_r<NB0, R % NB0, Ring<zs_abs(S0)>>(w0, wring_a + R0, rn + zs_abs(S0) * (S0 > 0 ? lpp : lpm));
-      if constexpr (NOB > 1) zemit_r<NB1, R % NB1, Ring<zs_abs(S1)>>(w1, wring_a + R1, rn + zs_abs(S1) * (S1 > 0 ? lpp : lpm));
-      if constexpr (NOB > 2) zemit_r<NB2, R % NB2, Ring<zs_abs(S2)>>(w2, wring_a + R2, rn + zs_abs(S2) * (S2 > 0 ? lpp : lpm));
-      if constexpr (NOB > 3) zemit_r<NB3, R % NB3, Ring<zs_abs(S3)>>(w3, wring_a + R3, rn + zs_abs(S3) * (S3 > 0 ? lpp : lpm));
-      zemit_r<NBP, R % NBP, PR>(wq, pring_a, rn + ASP * (SP > 0 ? lpp : lpm));
+      if constexpr (!HALF) {
+        // emit the completed cells (block rn + AS l' of each form); the window slides by rotation
+        zemit_r<NB0, R % NB0, Ring<zs_abs(S0)>>(w0, wring_a + R0, rn + zs_abs(S0) * (S0 > 0 ? lpp : lpm));
+        if constexpr (NOB > 1) zemit_r<NB1, R % NB1, Ring<zs_abs(S1)>>(w1, wring_a + R1, rn + zs_abs(S1) * (S1 > 0 ? lpp : lpm));
+        if constexpr (NOB > 2) zemit_r<NB2, R % NB2, Ring<zs_abs(S2)>>(w2, wring_a + R2, rn + zs_abs(S2) * (S2 > 0 ? lpp : lpm));
+        if constexpr (NOB > 3) zemit_r<NB3, R % NB3, Ring<zs_abs(S3)>>(w3, wring_a + R3, rn + zs_abs(S3) * (S3 > 0 ? lpp : lpm));
+        zemit_r<NBP, R % NBP, PR>(wq, pring_a, rn + ASP * (SP > 0 ? lpp : lpm));
+      }
       // XY slot row y: 8 consecutive z (partial over x-tiles)
       ptx::red_global_add_if(xyrow + 8 * rn, yzmine, xyrow != nullptr && z + lane < p.N && yzmine != 0);
       __syncwarp();
@@ -647,11 +710,19 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), 1) zstream_kernel(const __gri
       if (++pw == NW) pw = 0;
     };
     auto end_emit = [&]<int R>(const int rn_end) {
+      if constexpr (HALF) {
+        zemit_group_tail<S0, VX, WS0, Ring<zs_abs(S0)>>(w0, wring_a + R0, rn_end + zs_abs(S0) * (S0 > 0 ? lpp : lpm));
+        if constexpr (NOB > 1) zemit_group_tail<S1, VX, WS1, Ring<zs_abs(S1)>>(w1, wring_a + R1, rn_end + zs_abs(S1) * (S1 > 0 ? lpp : lpm));
+        if constexpr (NOB > 2) zemit_group_tail<S2, VX, WS2, Ring<zs_abs(S2)>>(w2, wring_a + R2, rn_end + zs_abs(S2) * (S2 > 0 ? lpp : lpm));
+        if constexpr (NOB > 3) zemit_group_tail<S3, VX, WS3, Ring<zs_abs(S3)>>(w3, wring_a + R3, rn_end + zs_abs(S3) * (S3 > 0 ? lpp : lpm));
+        zemit_group_tail<SP, VX, WSP, PR>(wq, pring_a, rn_end + ASP * (SP > 0 ? lpp : lpm));
+      } else {
       zemit_all_r<S0, VX, NB0, R % NB0, Ring<zs_abs(S0)>>(w0, wring_a + R0, rn_end + zs_abs(S0) * (S0 > 0 ? lpp : lpm));
       if constexpr (NOB > 1) zemit_all_r<S1, VX, NB1, R % NB1, Ring<zs_abs(S1)>>(w1, wring_a + R1, rn_end + zs_abs(S1) * (S1 > 0 ? lpp : lpm));
       if constexpr (NOB > 2) zemit_all_r<S2, VX, NB2, R % NB2, Ring<zs_abs(S2)>>(w2, wring_a + R2, rn_end + zs_abs(S2) * (S2 > 0 ? lpp : lpm));
       if constexpr (NOB > 3) zemit_all_r<S3, VX, NB3, R % NB3, Ring<zs_abs(S3)>>(w3, wring_a + R3, rn_end + zs_abs(S3) * (S3 > 0 ? lpp : lpm));
       zemit_all_r<SP, VX, NBP, R % NBP, PR>(wq, pring_a, rn_end + ASP * (SP > 0 ? lpp : lpm));
+      }
     };
     static_assert(ZU == 1 || ZU == 4, "the step loop is written for 1 or 4 phases");
     int rn = 0;
@@ -736,12 +807,12 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();   // project_stream.cu
 #endif
 
 #ifndef DPM_ZS_NW6
-#define DPM_ZS_NW6 8   // warps (= image rows) per CTA at orders 5-6 (255 registers, 4-plane fold groups)
+#define DPM_ZS_NW6 (DPM_ZS_HALF ? 12 : 8)   // warps (= image rows) per CTA at orders 5-6
 #endif
 template <typename T, int K> struct ZCfg {
   static constexpr int VX = 8;
-  static constexpr int NW = K >= 5 ? DPM_ZS_NW6 : 12;
-  static constexpr int FMAMASK = K >= 5 && NW > 8 ? DPM_ZS_FMAMASK6 : DPM_ZS_FMAMASK;
+  static constexpr int NW = K >= 5 ? DPM_ZS_NW6 : DPM_ZS_NW34;
+  static constexpr int FMAMASK = K >= 5 && NW > 8 && !DPM_ZS_HALF ? DPM_ZS_FMAMASK6 : DPM_ZS_FMAMASK;
   static constexpr int STAGE = 32 * VX * NW * 8 * (int)sizeof(T);
   static constexpr int RINGS = NW * ZGeo<T, K, NW, VX, 1>::WARP_RING * 4 + 8 * 200 * 4;
   static constexpr int FIT = (225 * 1024 - RINGS) / STAGE;
