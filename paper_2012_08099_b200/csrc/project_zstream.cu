@@ -61,6 +61,9 @@
 #ifndef DPM_ZS_HALF
 #define DPM_ZS_HALF 1   // orders 5-6: windows spanning one fold group, emitted per group, 12 warps (v33)
 #endif
+#ifndef DPM_ZS_RUN_MB
+#define DPM_ZS_RUN_MB (1 << 20)   // image sets up to this size (MB): equal contiguous runs; larger: round robin (x34: runs always win)
+#endif
 #ifndef DPM_ZS_HALF_MINK
 #define DPM_ZS_HALF_MINK 5   // lowest order that uses the group-wise windows
 #endif
@@ -864,7 +867,7 @@ static int launch_zs(const dpm_volume_desc* d, const void* vox, const ImageSet& 
   int64_t img_bytes = 0;
   for (int k = 0; k < s.n_img; ++k) img_bytes += s.W[k] * s.H[k] * 4 * d->B;
   const int64_t G_ = sms;
-  if (img_bytes <= (48ll << 20) || p.ncol * p.ns < 4 * G_) {
+  if (img_bytes <= ((int64_t)DPM_ZS_RUN_MB << 20) || p.ncol * p.ns < 4 * G_) {
     p.run_mode = 1;
     p.zsplit = 1;
   } else {
