@@ -61,6 +61,10 @@
 #ifndef DPM_ZS_HALF
 #define DPM_ZS_HALF 1   // orders 5-6: windows spanning one fold group, emitted per group, 12 warps (v33)
 #endif
+#ifndef DPM_ZS_CTAS6
+#define DPM_ZS_CTAS6 1   // CTAs per SM at orders 5-6
+#endif
+__host__ __device__ constexpr int zs_ctas(int K) { return K >= 5 ? DPM_ZS_CTAS6 : 1; }
 #ifndef DPM_ZS_RUN_MB
 #define DPM_ZS_RUN_MB (1 << 20)   // image sets up to this size (MB): equal contiguous runs; larger: round robin (x34: runs always win)
 #endif
@@ -440,7 +444,7 @@ template <int NW> __device__ __forceinline__ void zs_sync() {
 }
 
 template <typename T, int K, int NW, int VX, int STAGES, int FMAMASK>
-__global__ void __launch_bounds__(32 * (NW + ZPW), 1) zstream_kernel(const __grid_constant__ CUtensorMap tmap, const ZParams p) {
+__global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(const __grid_constant__ CUtensorMap tmap, const ZParams p) {
   using G = ZGeo<T, K, NW, VX, STAGES>;
   using V = typename ZVec<T, VX>::type;
   constexpr int NOB = G::NOB, SX = G::SX;
@@ -818,7 +822,7 @@ template <typename T, int K> struct ZCfg {
   static constexpr int FMAMASK = K >= 5 && NW > 8 && !DPM_ZS_HALF ? DPM_ZS_FMAMASK6 : DPM_ZS_FMAMASK;
   static constexpr int STAGE = 32 * VX * NW * 8 * (int)sizeof(T);
   static constexpr int RINGS = NW * ZGeo<T, K, NW, VX, 1>::WARP_RING * 4 + 8 * 200 * 4;
-  static constexpr int FIT = (225 * 1024 - RINGS) / STAGE;
+  static constexpr int FIT = ((zs_ctas(K) == 1 ? 225 : 226 / zs_ctas(K)) * 1024 - RINGS) / STAGE;
   static constexpr int STAGES = FIT > 6 ? 6 : FIT;
 };
 
@@ -866,7 +870,7 @@ static int launch_zs(const dpm_volume_desc* d, const void* vox, const ImageSet& 
   // over z-split segments (chosen for balance, segments >= 8 steps)
   int64_t img_bytes = 0;
   for (int k = 0; k < s.n_img; ++k) img_bytes += s.W[k] * s.H[k] * 4 * d->B;
-  const int64_t G_ = sms;
+  const int64_t G_ = (int64_t)sms * zs_ctas(K);
   if (img_bytes <= ((int64_t)DPM_ZS_RUN_MB << 20) || p.ncol * p.ns < 4 * G_) {
     p.run_mode = 1;
     p.zsplit = 1;
