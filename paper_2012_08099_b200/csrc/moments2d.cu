@@ -89,8 +89,13 @@ __device__ __forceinline__ void profile_block(const M2Params& p, int64_t b, int6
   }
 }
 
+#ifdef DPM_M2_MINB
+#define DPM_M2_BOUNDS __launch_bounds__(M2_THREADS, DPM_M2_MINB)   // register cap for A/B builds
+#else
+#define DPM_M2_BOUNDS __launch_bounds__(M2_THREADS)
+#endif
 template <int K, int JB>
-__global__ void __launch_bounds__(M2_THREADS) moments2d_kernel(M2Params p) {
+__global__ void DPM_M2_BOUNDS moments2d_kernel(M2Params p) {
   using LP = Limbs<JB>;
   constexpr int NT = LP::off(K + 1);        // total limbs across q = 0..K
   constexpr int NTP = (NT + 3) & ~3;        // padded to uint4
