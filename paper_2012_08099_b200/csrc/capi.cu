@@ -57,6 +57,48 @@ static int check_desc(const dpm_volume_desc* d) {
   return DPM_OK;
 }
 
+struct ZeroList {
+  uint8_t* p[DPM_MAX_IMAGES + 2];
+  uint64_t bytes[DPM_MAX_IMAGES + 2];
+  int n;
+};
+
+// grid-stride zeroing of up to 9 buffers (16-byte stores, byte tail); starts
+// its dependent (PDL) immediately
+__global__ void zero_kernel(const ZeroList z) {
+  pdl_trigger();
+  const size_t stride = (size_t)gridDim.x * blockDim.x, t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int b = 0; b < z.n; ++b) {
+    uint4* q = reinterpret_cast<uint4*>(z.p[b]);
+    const size_t n16 = z.bytes[b] / 16;
+    for (size_t i = t0; i < n16; i += stride) q[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (size_t i = n16 * 16 + t0; i < z.bytes[b]; i += stride) z.p[b][i] = 0;
+  }
+}
+
+static int zero_list_async(const ZeroList& z, cudaStream_t st) {
+  size_t total = 0;
+  for (int b = 0; b < z.n; ++b) total += z.bytes[b];
+  if (total == 0) return DPM_OK;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t want = (total / 16 + 255) / 256;
+  const unsigned grid = (unsigned)(want < (size_t)sms * 4 ? (want > 0 ? want : 1) : (size_t)sms * 4);
+  zero_kernel<<<grid, 256, 0, st>>>(z);
+  note_launches(1);
+  DPM_CUDA_CHECK_LAUNCH();
+  return DPM_OK;
+}
+
+int zero_async(void* p, size_t bytes, cudaStream_t st) {
+  ZeroList z;
+  z.n = 1;
+  z.p[0] = static_cast<uint8_t*>(p);
+  z.bytes[0] = bytes;
+  return zero_list_async(z, st);
+}
+
 static int check_order(int order) { return (order >= 3 && order <= DPM_MAX_ORDER) ? DPM_OK : DPM_EINVAL; }
 
 // Moments-pipeline layout.  Wide volumes use layout T: the
@@ -275,14 +317,19 @@ int dpm_project_profile(const dpm_volume_desc* desc, const void* d_voxels, int o
   const int n_img = num_images(order);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   ImageSet s = make_set(desc, n_img, d_images, true);
+  ZeroList z;
+  z.n = 0;
   for (int k = 0; k < n_img; ++k) {
     if (k == DPM_IMG_ZX) continue;
     if (!s.img[k]) return DPM_EINVAL;
-    if (cudaMemsetAsync(s.img[k], 0, (size_t)(s.W[k] * s.H[k] * desc->B) * sizeof(uint32_t), st) != cudaSuccess)
-      return DPM_ECUDA;
+    z.p[z.n] = reinterpret_cast<uint8_t*>(s.img[k]);
+    z.bytes[z.n++] = (uint64_t)(s.W[k] * s.H[k] * desc->B) * sizeof(uint32_t);
   }
   const ProfGeom pg = profile_geom(desc, order);
-  if (cudaMemsetAsync(d_profile, 0, (size_t)(pg.WQ * desc->B) * sizeof(uint64_t), st) != cudaSuccess) return DPM_ECUDA;
+  z.p[z.n] = reinterpret_cast<uint8_t*>(d_profile);
+  z.bytes[z.n++] = (uint64_t)(pg.WQ * desc->B) * sizeof(uint64_t);
+  rc = zero_list_async(z, st);   // one launch; the projection kernel starts while it drains (PDL)
+  if (rc) return rc;
   return project_profile_launch(desc, d_voxels, order, d_images, d_profile, st);
 }
 
@@ -294,8 +341,8 @@ int dpm_moments2d_profile(const dpm_volume_desc* desc, int order, const uint32_t
   if (check_order(order) || !d_images || !d_profile || !d_acc) return DPM_EINVAL;
   const int n_img = num_images(order);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (cudaMemsetAsync(d_acc, 0, (size_t)(desc->B * n_img * n2d(order) * 4) * sizeof(uint64_t), st) != cudaSuccess)
-    return DPM_ECUDA;
+  rc = zero_async(d_acc, (size_t)(desc->B * n_img * n2d(order) * 4) * sizeof(uint64_t), st);
+  if (rc) return rc;
   return moments2d_profile_launch(desc, order, d_images, d_profile, d_acc, st);
 }
 
@@ -309,9 +356,14 @@ int dpm_moments2d_profile_derive(const dpm_volume_desc* desc, int order, const u
     return DPM_EINVAL;
   const int n_img = num_images(order);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (cudaMemsetAsync(d_acc, 0, (size_t)(desc->B * n_img * n2d(order) * 4) * sizeof(uint64_t), st) != cudaSuccess ||
-      cudaMemsetAsync(d_counters, 0, (size_t)desc->B * sizeof(uint32_t), st) != cudaSuccess)
-    return DPM_ECUDA;
+  ZeroList z;
+  z.n = 2;
+  z.p[0] = reinterpret_cast<uint8_t*>(d_acc);
+  z.bytes[0] = (uint64_t)(desc->B * n_img * n2d(order) * 4) * sizeof(uint64_t);
+  z.p[1] = reinterpret_cast<uint8_t*>(d_counters);
+  z.bytes[1] = (uint64_t)desc->B * sizeof(uint32_t);
+  rc = zero_list_async(z, st);
+  if (rc) return rc;
   FusedOut f;
   f.cnt = d_counters;
   f.i128 = d_m3d_i128;
@@ -353,11 +405,12 @@ static int moments_partial_impl(const dpm_volume_desc* desc, const void* d_voxel
                       (fused ? align256((size_t)desc->B * sizeof(unsigned int)) : 0);
   char* z0 = single ? reinterpret_cast<char*>(prof) : base;
   const size_t zb = (single ? 0 : ib) + tail + (acc_adjacent ? acc_bytes_of(desc, order) : 0);
-  if (cudaMemsetAsync(z0, 0, zb, st) != cudaSuccess) return DPM_ECUDA;
+  reset_launches();
   if (!acc_adjacent && zero_acc &&
       cudaMemsetAsync(d_acc, 0, (size_t)(desc->B * n_img * n2d(order) * 4) * sizeof(uint64_t), st) != cudaSuccess)
     return DPM_ECUDA;
-  reset_launches();
+  rc = zero_async(z0, zb, st);   // last before the projection kernel: it starts while this drains (PDL)
+  if (rc) return rc;
   rc = project_profile_launch(desc, d_voxels, order, imgs, prof, st, !single);
   if (rc) return rc;
   return moments2d_profile_launch(desc, order, imgs, prof, d_acc, st, fused);
@@ -536,8 +589,9 @@ int dpm_moments(const dpm_volume_desc* desc, const void* d_voxels, int order, vo
     // small uint8 volumes (<= 128 wide and deep, order 3): one memset of
     // [counters | acc] and ONE launch for projection, moments and epilogue
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (cudaMemsetAsync(f.cnt, 0, cbytes + acc_bytes_of(desc, order), st) != cudaSuccess) return DPM_ECUDA;
     reset_launches();
+    rc = zero_async(f.cnt, cbytes + acc_bytes_of(desc, order), st);
+    if (rc) return rc;
     bool handled = false;
     rc = launch_fused_batch(desc, d_voxels, order, acc, f.cnt, d_m3d_i128, d_m3d_f64, d_status, st, &handled);
     if (rc || handled) return rc;

@@ -94,6 +94,41 @@ __host__ __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { retur
 }  // namespace dpm
 
 namespace dpm {
+// Programmatic dependent launch (PDL).  The pipeline's kernels are launched
+// with programmatic stream serialisation, so a kernel starts while its
+// predecessor drains: it runs its prologue (shared-memory setup, barrier
+// init, the first TMA loads of the VOLUME, which earlier stream work
+// produced) and calls pdl_wait() before it touches anything the predecessor
+// writes (zeroed images / accumulators, images to reduce).  Predecessors call
+// pdl_trigger() early.  Without a programmatic dependency both are no-ops.
+// DPM_PDL=0 launches everything with plain stream order (A/B).
+#ifndef DPM_PDL
+#define DPM_PDL 1
+#endif
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... ExpTypes, typename... ActTypes>
+inline cudaError_t launch_pdl(void (*kern)(ExpTypes...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              ActTypes&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = DPM_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<ActTypes&&>(args)...);
+}
+
+// zero `bytes` at `p` (256-byte aligned) with a kernel that lets its
+// dependent start right away (cudaMemsetAsync is not a kernel, so it cannot
+// take part in PDL); counts as one launch
+int zero_async(void* p, size_t bytes, cudaStream_t st);
+
 // Dynamic shared-memory opt-in of one kernel, set once per DEVICE (the
 // attribute lives in that device's context; a process-wide once-flag would
 // leave a second GPU unconfigured).  `mask` is the kernel's own bit set of

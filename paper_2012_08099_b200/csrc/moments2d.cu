@@ -110,7 +110,9 @@ __global__ void DPM_M2_BOUNDS moments2d_kernel(M2Params p) {
   const int64_t b = blockIdx.x / per_vol;
   int64_t r = blockIdx.x - b * per_vol;
   const int tid = threadIdx.x;
+  pdl_trigger();
   if (r >= per_img) {
+    pdl_wait();   // the profile is complete once the projection grid is
     profile_block<K>(p, b, r - per_img, tid);
   } else {
   int k = 0;
@@ -136,6 +138,7 @@ __global__ void DPM_M2_BOUNDS moments2d_kernel(M2Params p) {
     for (int l = NT; l < NTP; ++l) table[rr][l] = 0;
   }
   __syncthreads();
+  pdl_wait();   // images complete (the row-power table above overlapped the projection's tail)
 
   const int64_t i = cb * M2_THREADS + tid;
   uint64_t acc[NTP];
@@ -238,7 +241,7 @@ static int launch_kj(dim3 grid, cudaStream_t st, const M2Params& p) {
   constexpr size_t bytes = t_bytes > r_bytes ? t_bytes : r_bytes;
   static std::atomic<uint64_t> attr_mask{0};
   if (ensure_smem(moments2d_kernel<K, JB>, bytes, attr_mask)) return DPM_ECUDA;
-  moments2d_kernel<K, JB><<<grid, M2_THREADS, bytes, st>>>(p);
+  if (launch_pdl(moments2d_kernel<K, JB>, grid, dim3(M2_THREADS), bytes, st, p) != cudaSuccess) return DPM_ECUDA;
   return DPM_OK;
 }
 

@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) fused_batch_kernel(const __g
   // end of this CTA's rows of volume vb: partial moments -> limb accumulator;
   // the CTA that completes the volume runs the epilogue
   auto volume_end = [&](int64_t vb, int32_t rows_done) {
+    pdl_wait();   // accumulator and counters zeroed by the preceding kernel (no-op after the first volume)
     flush_pq();
     __syncthreads();
     // profile cells of this thread (read and re-zero the CTA row)
@@ -417,7 +418,8 @@ static int launch_fb(const dpm_volume_desc* d, const void* vox, const FBParams& 
   static std::atomic<uint64_t> attr_mask{0};
   if (ensure_smem(fused_batch_kernel<NW>, G::SMEM, attr_mask)) return DPM_ECUDA;
   const int grid = (int)imin64((int64_t)sms * G::CTAS, p.total);
-  fused_batch_kernel<NW><<<grid, G::THREADS, G::SMEM, st>>>(map, p);
+  if (launch_pdl(fused_batch_kernel<NW>, dim3(grid), dim3(G::THREADS), G::SMEM, st, map, p) != cudaSuccess)
+    return DPM_ECUDA;
   return DPM_OK;
 }
 

@@ -524,7 +524,9 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
     }
   }
   if (lane == 0 && w < NW) segs[w].first(p);
+  pdl_trigger();    // the moments launch may start its prologue while this grid drains
   __syncthreads();
+  pdl_wait();       // images / profile zeroed by the preceding kernel (the first TMA loads are in flight)
   if constexpr (ZPW) {
     if (w == NW) {   // producer warp: refill each stage as soon as every compute warp released it
       if (lane == 0) {
@@ -890,7 +892,9 @@ static int launch_zs(const dpm_volume_desc* d, const void* vox, const ImageSet& 
   if (ensure_smem(zstream_kernel<T, K, NW, VX, S, C::FMAMASK>, G::SMEM, attr_mask)) return DPM_ECUDA;
   const int64_t units = p.run_mode ? p.ncol * p.ns : p.ncol * p.zsplit;
   const int grid = (int)imin64(G_, units);
-  zstream_kernel<T, K, NW, VX, S, C::FMAMASK><<<grid, 32 * (NW + ZPW), G::SMEM, st>>>(map, p);
+  if (launch_pdl(zstream_kernel<T, K, NW, VX, S, C::FMAMASK>, dim3(grid), dim3(32 * (NW + ZPW)), G::SMEM, st, map, p) !=
+      cudaSuccess)
+    return DPM_ECUDA;
   return DPM_OK;
 }
 
