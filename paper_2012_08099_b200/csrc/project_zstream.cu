@@ -65,6 +65,12 @@
 #define DPM_ZS_CTAS6 1   // CTAs per SM at orders 5-6
 #endif
 __host__ __device__ constexpr int zs_ctas(int K) { return K >= 5 ? DPM_ZS_CTAS6 : 1; }
+#ifndef DPM_ZS_XY_SMEM
+#define DPM_ZS_XY_SMEM 1   // XY-slot plane sums through a per-warp shared word each instead of lane selects (x37)
+#endif
+#ifndef DPM_ZS_SLEEP
+#define DPM_ZS_SLEEP 0   // suspend-time hint (ns) of the stage waits; 0 = plain try_wait polling
+#endif
 #ifndef DPM_ZS_RUN_MB
 #define DPM_ZS_RUN_MB (1 << 20)   // image sets up to this size (MB): equal contiguous runs; larger: round robin (x34: runs always win)
 #endif
@@ -144,7 +150,7 @@ template <typename T, int K, int NW, int VX, int STAGES> struct ZGeo {
   static constexpr int WARP_RING = ring_off(NOB);               // words per warp
   static constexpr int PR_WORDS = PRing<ASP, STAGES>::WORDS;
   static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + (size_t)NW * WARP_RING * 4 + PR_WORDS * 4 + 8 +
-                                 2 * STAGES * 8 + 128 + 64 * NW + 96 * STAGES;   // + producer state, warps' cursors, stage cursors
+                                 2 * STAGES * 8 + 128 + 64 * NW + 96 * STAGES + 32 * NW + 16;   // + producer state, cursors, XY-slot sums
 };
 
 // ---- lane vectors ------------------------------------------------------------
@@ -472,6 +478,7 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
   ZProd* prods = reinterpret_cast<ZProd*>(segs + NW);        // [STAGES] per-stage cursors (ZLAST)
   uint32_t* rel = reinterpret_cast<uint32_t*>(prods + STAGES);   // [STAGES] release counters (ZLAST)
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  uint32_t* xyv = rel + STAGES + 8 * w;                          // [NW][8] this warp's XY-slot plane sums
 
   if (w < NW)
     for (int i = tid; i < NW * G::WARP_RING + G::PR_WORDS; i += 32 * NW) rings[i] = 0;
@@ -613,7 +620,8 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
         ptx::mbar_wait_addr(bar_a + 8u * (uint32_t)(STAGES + kl), phl);
         issue();
       }
-      ptx::mbar_wait_addr(bar_a + 8u * (uint32_t)k, ph);
+      if constexpr (DPM_ZS_SLEEP > 0) ptx::mbar_wait_addr_sleep(bar_a + 8u * (uint32_t)k, ph, DPM_ZS_SLEEP);
+      else ptx::mbar_wait_addr(bar_a + 8u * (uint32_t)k, ph);
       // step g's stage was refilled only after every warp released step g - STAGES:
       // profile blocks <= rn - STAGES are complete; warp g mod NW flushes that one
       if (w == pw && rn >= STAGES && lane < 8) {
@@ -652,7 +660,8 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
             sm = (P[gg][0] + P[gg][1] + P[gg][2]) + (P[gg][3] + P[gg][4]) + (P[gg][5] + P[gg][6]) + P[gg][7];
           }
           const uint32_t r = __reduce_add_sync(0xffffffffu, sm);
-          yzmine = lane == GP * h + gg ? r : yzmine;
+          if constexpr (DPM_ZS_XY_SMEM) ptx::sts_u32(ptx::smem_addr(xyv + GP * h + gg), r);   // uniform value, one word
+          else yzmine = lane == GP * h + gg ? r : yzmine;
         }
         // YZ slot: x-sums over z
         #pragma unroll
@@ -692,6 +701,10 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
         zemit_r<NBP, R % NBP, PR>(wq, pring_a, rn + ASP * (SP > 0 ? lpp : lpm));
       }
       // XY slot row y: 8 consecutive z (partial over x-tiles)
+      if constexpr (DPM_ZS_XY_SMEM) {
+        __syncwarp();
+        yzmine = lane < 8 ? ptx::lds_u32(ptx::smem_addr(xyv + (lane & 7))) : 0u;
+      }
       ptx::red_global_add_if(xyrow + 8 * rn, yzmine, xyrow != nullptr && z + lane < p.N && yzmine != 0);
       __syncwarp();
       // the ring block this step completed: lanes 8j..8j+7 flush form j's 8 cells

@@ -41,6 +41,18 @@ __device__ __forceinline__ void mbar_wait_addr(uint32_t bar, uint32_t phase) {
       : "memory");
 }
 
+// the same with a suspend-time hint (ns): the warp sleeps until the phase
+// completes or the hint expires instead of re-polling (no issue slots spent)
+__device__ __forceinline__ void mbar_wait_addr_sleep(uint32_t bar, uint32_t phase, uint32_t hint_ns) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, %2;\n\t"
+      "@!done bra WAITS_%=;\n\t}" ::"r"(bar),
+      "r"(phase), "r"(hint_ns)
+      : "memory");
+}
+
 // ---- TMA -----------------------------------------------------------------------
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");

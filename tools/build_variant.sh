@@ -9,9 +9,10 @@ B=$ROOT/tools/ab/build_$NAME
 rm -rf "$B"; mkdir -p "$B"
 for f in "$SRC"/*.cu; do
   nvcc $FLAGS -std=c++20 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC \
-    -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr -c "$f" -o "$B/$(basename "${f%.cu}").o" 2>/dev/null &
+    -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr -c "$f" -o "$B/$(basename "${f%.cu}").o" 2>"$B/$(basename "${f%.cu}").log" &
 done
 wait
+if grep -l " error" "$B"/*.log >/dev/null 2>&1; then grep -h " error" "$B"/*.log | head -5; exit 1; fi
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$ROOT/tools/ab/lib_$NAME.so" "$B"/*.o -lcudart_static -Xcompiler -fvisibility=hidden
 rm -rf "$B"
 echo "built tools/ab/lib_$NAME.so"
