@@ -77,6 +77,10 @@ __host__ __device__ constexpr int zs_ctas(int K) { return K >= 5 ? DPM_ZS_CTAS6 
 #ifndef DPM_ZS_HALF_MINK
 #define DPM_ZS_HALF_MINK 5   // lowest order that uses the group-wise windows
 #endif
+#ifndef DPM_ZS_SPLIT
+#define DPM_ZS_SPLIT 0   // group-wise windows: fetch each step as two half boxes with their own barriers
+#endif
+__host__ __device__ constexpr int zs_spl(int K) { return (DPM_ZS_SPLIT && DPM_ZS_HALF && K >= DPM_ZS_HALF_MINK) ? 2 : 1; }
 #ifndef DPM_ZS_NW34
 #define DPM_ZS_NW34 12       // warps per CTA at orders 3-4
 #endif
@@ -150,7 +154,7 @@ template <typename T, int K, int NW, int VX, int STAGES> struct ZGeo {
   static constexpr int WARP_RING = ring_off(NOB);               // words per warp
   static constexpr int PR_WORDS = PRing<ASP, STAGES>::WORDS;
   static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + (size_t)NW * WARP_RING * 4 + PR_WORDS * 4 + 8 +
-                                 2 * STAGES * 8 + 128 + 64 * NW + 96 * STAGES + 32 * NW + 16;   // + producer state, cursors, XY-slot sums
+                                 4 * STAGES * 8 + 128 + 64 * NW + 96 * STAGES + 32 * NW + 16;   // + producer state, cursors, XY-slot sums
 };
 
 // ---- lane vectors ------------------------------------------------------------
@@ -419,8 +423,9 @@ struct ZSeg {
 // (step g's refill is issued by warp g mod NW), so no warp is slower than the rest
 struct ZProd {
   ZSeg seg;
-  int32_t n, k;          // next step to issue (within seg), its stage
+  int32_t n, k;          // next step to issue (within seg), its stage (sub-stage with DPM_ZS_SPLIT)
   int32_t xt, yg, b;     // decoded column of seg
+  int32_t hh;            // next half of step n (DPM_ZS_SPLIT)
 };
 __device__ __forceinline__ void zdecode(const ZParams& p, int64_t col, int32_t& xt, int32_t& yg, int32_t& b) {
   xt = (int32_t)(col % p.n_xt);
@@ -464,6 +469,14 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
   // folded on the ALU pipe, 2 (fewer live registers) when those go to the FMA pipe
   constexpr int GP = (NOB <= 2 || (FMAMASK & 12) == 12) && ((FMAMASK & 16) || ASP == 1) ? 2 : DPM_ZS_GP;
   constexpr bool HALF = DPM_ZS_HALF && K >= DPM_ZS_HALF_MINK;   // group-wise windows (see zemit_group)
+  // DPM_ZS_SPLIT: each step's box is fetched as two half boxes of 4 planes with
+  // their own barriers, one per fold group: a half-stage is released (and
+  // refilled) after its group, half a step earlier than a whole stage
+  constexpr int SPL = zs_spl(K);
+  static_assert(SPL == 1 || (HALF && GP == 4), "half-box stages need the 4-plane group-wise windows");
+  constexpr int NSUB = STAGES * SPL;
+  constexpr uint32_t SUB_BYTES = G::STAGE_BYTES / SPL;
+  constexpr int PPS = 8 / SPL;   // planes per (sub-)stage
   using PR = PRing<ASP, STAGES>;
   constexpr uint32_t R0 = G::ring_off(0) * 4, R1 = G::ring_off(1) * 4, R2 = G::ring_off(2) * 4,
                      R3 = G::ring_off(3) * 4;
@@ -472,8 +485,8 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
   uint32_t* rings = reinterpret_cast<uint32_t*>(smem + (size_t)STAGES * G::STAGE_BYTES);
   uint32_t* pring = rings + NW * G::WARP_RING;
   uint64_t* full = reinterpret_cast<uint64_t*>(pring + G::PR_WORDS + ((G::PR_WORDS & 1) ? 1 : 0));
-  uint64_t* empty = full + STAGES;
-  ZProd* prod = reinterpret_cast<ZProd*>(empty + STAGES);   // producer state (thread 0 only)
+  uint64_t* empty = full + NSUB;
+  ZProd* prod = reinterpret_cast<ZProd*>(empty + NSUB);     // producer state (thread 0 only)
   ZSeg* segs = reinterpret_cast<ZSeg*>(prod + 1);            // [NW] each warp's segment cursor
   ZProd* prods = reinterpret_cast<ZProd*>(segs + NW);        // [STAGES] per-stage cursors (ZLAST)
   uint32_t* rel = reinterpret_cast<uint32_t*>(prods + STAGES);   // [STAGES] release counters (ZLAST)
@@ -482,14 +495,16 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
 
   if (w < NW)
     for (int i = tid; i < NW * G::WARP_RING + G::PR_WORDS; i += 32 * NW) rings[i] = 0;
-  auto issue = [&]() {   // thread 0: the next step of the sequence into its stage
+  auto issue = [&]() {   // thread 0: the next step (half step with SPL = 2) of the sequence into its stage
     ZProd st = *prod;
     if (st.seg.done) return;
     const int k = st.k;
-    ptx::mbar_arrive_expect_tx(&full[k], G::STAGE_BYTES);
-    ptx::tma_load_4d_hint(stages + (size_t)k * G::STAGE_BYTES, &tmap, &full[k], st.xt * SX, st.yg * NW, st.n * 8,
+    ptx::mbar_arrive_expect_tx(&full[k], SUB_BYTES);
+    ptx::tma_load_4d_hint(stages + (size_t)k * SUB_BYTES, &tmap, &full[k], st.xt * SX, st.yg * NW, st.n * 8 + PPS * st.hh,
                           st.b, ptx::policy_evict_first());
-    st.k = k + 1 == STAGES ? 0 : k + 1;
+    st.k = k + 1 == NSUB ? 0 : k + 1;
+    if (SPL == 2 && st.hh == 0) { st.hh = 1; *prod = st; return; }
+    st.hh = 0;
     if (++st.n == st.seg.n1) {
       st.seg.next(p);
       if (!st.seg.done) { st.n = st.seg.n0; zdecode(p, st.seg.col, st.xt, st.yg, st.b); }
@@ -516,10 +531,11 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
   };
   if (tid == 0) {
     ptx::prefetch_tmap(&tmap);
-    for (int i = 0; i < STAGES; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&empty[i], NW); }
+    for (int i = 0; i < NSUB; ++i) { ptx::mbar_init(&full[i], 1); ptx::mbar_init(&empty[i], NW); }
     ptx::fence_barrier_init();
     ZProd st;
     st.k = 0;
+    st.hh = 0;
     st.seg.first(p);
     if (!st.seg.done) { st.n = st.seg.n0; zdecode(p, st.seg.col, st.xt, st.yg, st.b); }
     if constexpr (ZLAST) {
@@ -527,7 +543,7 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
       for (int h = 0; h < STAGES; ++h) issue_stage(h);
     } else {
       *prod = st;
-      for (int h = 0; h < STAGES; ++h) issue();
+      for (int h = 0; h < NSUB; ++h) issue();
     }
   }
   if (lane == 0 && w < NW) segs[w].first(p);
@@ -542,7 +558,7 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
         while (!prod->seg.done) {
           ptx::mbar_wait_addr(ptx::smem_addr(empty) + 8u * (uint32_t)kk, ph);
           issue();
-          if (++kk == STAGES) { kk = 0; ph ^= 1u; }
+          if (++kk == NSUB) { kk = 0; ph ^= 1u; }
         }
       }
       return;
@@ -565,6 +581,7 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
 #define DPM_ZS_ZLAG (K >= 6 ? 2 : 1)   // measured best per order (x26)
 #endif
   constexpr int ZLAG = STAGES >= 4 ? DPM_ZS_ZLAG : 1;
+  constexpr int ZLAGS = ZLAG * SPL;   // the same lag in sub-stages
   static_assert(sizeof(ZProd) <= 96, "stage cursor budget (ZGeo::SMEM)");
   int k = 0, pw = 0, kl = 0, lagc = 0;
   uint32_t ph = 0, phl = 0;
@@ -612,18 +629,24 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
     for (int i = 0; i < VX; ++i) cs[i] = 0;
 
     // one step (8 planes) at window phase R = rn mod ZU
-    auto step = [&]<int R>(const int rn) {
-      if (!ZPW && !ZLAST && tid == 0 && lagc >= ZLAG) {
-        // producer: once every warp released step g - ZLAG, refill its stage with
-        // step g - ZLAG + STAGES.  The lag leaves the other warps ZLAG - 1 steps of
-        // slack before the producer has to wait for the slowest of them.
-        ptx::mbar_wait_addr(bar_a + 8u * (uint32_t)(STAGES + kl), phl);
-        issue();
+    // the producer (thread 0): once every warp released sub-stage g - ZLAGS,
+    // refill it with sub-step g - ZLAGS + NSUB.  The lag leaves the other warps
+    // ZLAGS - 1 sub-steps of slack before the producer waits for the slowest.
+    auto produce = [&]() {
+      if (!ZPW && !ZLAST && tid == 0) {
+        if (lagc >= ZLAGS) {
+          ptx::mbar_wait_addr(bar_a + 8u * (uint32_t)(NSUB + kl), phl);
+          issue();
+          if (++kl == NSUB) { kl = 0; phl ^= 1u; }
+        } else {
+          ++lagc;
+        }
       }
-      if constexpr (DPM_ZS_SLEEP > 0) ptx::mbar_wait_addr_sleep(bar_a + 8u * (uint32_t)k, ph, DPM_ZS_SLEEP);
-      else ptx::mbar_wait_addr(bar_a + 8u * (uint32_t)k, ph);
-      // step g's stage was refilled only after every warp released step g - STAGES:
-      // profile blocks <= rn - STAGES are complete; warp g mod NW flushes that one
+    };
+    // step g's (last) sub-stage was refilled only after every warp released
+    // step g - STAGES: profile blocks <= rn - STAGES are complete; warp g mod NW
+    // flushes that one
+    auto flush_profile_block = [&](const int rn) {
       if (w == pw && rn >= STAGES && lane < 8) {
         const int blk = rn - STAGES;
         const uint32_t a = pring_a + 4u * (uint32_t)(PR::idx(blk) + lane * PR::RP);
@@ -632,17 +655,47 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
         const int32_t i = pbase + 8 * blk + lane;
         if (v != 0 && i >= 0 && i < p.WQ) atomicAdd(prow + i, (unsigned long long)v);
       }
+    };
+    auto release = [&]() {   // this warp is done with (sub-)stage k
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (ZLAST) {   // the last of the NW warps to release stage k refills it
+          uint32_t old;
+          asm volatile("atom.shared.inc.u32 %0, [%1], %2;" : "=r"(old) : "r"(ptx::smem_addr(rel + k)), "r"((uint32_t)(NW - 1)) : "memory");
+          if (old == (uint32_t)(NW - 1)) issue_stage(k);
+        } else {
+          ptx::mbar_arrive_addr(bar_a + 8u * (uint32_t)(NSUB + k));
+        }
+      }
+      if (++k == NSUB) { k = 0; ph ^= 1u; }
+    };
+    // one step (8 planes) at window phase R = rn mod ZU
+    auto step = [&]<int R>(const int rn) {
       const int32_t z = 8 * (n0 + rn);
-      const uint32_t tile_a = stage_a + (uint32_t)k * G::STAGE_BYTES;
       uint32_t yzmine = 0;
+      uint32_t tile_a = 0;
+      if constexpr (SPL == 1) {
+        produce();
+        if constexpr (DPM_ZS_SLEEP > 0) ptx::mbar_wait_addr_sleep(bar_a + 8u * (uint32_t)k, ph, DPM_ZS_SLEEP);
+        else ptx::mbar_wait_addr(bar_a + 8u * (uint32_t)k, ph);
+        flush_profile_block(rn);
+        tile_a = stage_a + (uint32_t)k * G::STAGE_BYTES;
+      }
       #pragma unroll
       for (int h = 0; h < 8 / GP; ++h) {
+        if constexpr (SPL == 2) {   // group h = half-stage k
+          produce();
+          ptx::mbar_wait_addr(bar_a + 8u * (uint32_t)k, ph);
+          if (h == 1) flush_profile_block(rn);
+          tile_a = stage_a + (uint32_t)k * SUB_BYTES;
+        }
         uint32_t P[GP][VX];
         V draw[GP];
         #pragma unroll
         for (int gg = 0; gg < GP; ++gg) {
           const int t = GP * h + gg;
-          const V d = ptx::lds_vec<V>(tile_a + (uint32_t)(t * NW * SX * (int)sizeof(T)));
+          const int ts = SPL == 2 ? gg : t;   // plane within the (sub-)stage
+          const V d = ptx::lds_vec<V>(tile_a + (uint32_t)(ts * NW * SX * (int)sizeof(T)));
           draw[gg] = d;
           ZUnpack<T>::run(d, P[gg], z + t < p.N ? off_lane : 0, p.one << 16);
         }
@@ -679,6 +732,7 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
           if constexpr (NOB > 2) zfold<S2, VX, GP, (FMAMASK & 4) != 0, WS2>(w2, P, 0, p.one);
           if constexpr (NOB > 3) zfold<S3, VX, GP, (FMAMASK & 8) != 0, WS3>(w3, P, 0, p.one);
           zfold<SP, VX, GP, (FMAMASK & 16) != 0, WSP>(wq, P, 0, p.one);
+          if constexpr (SPL == 2) release();   // every value of this half-stage is in registers and used
           zemit_group<GP, WS0, Ring<zs_abs(S0)>>(w0, wring_a + R0, rn + zs_abs(S0) * (S0 > 0 ? lpp : lpm), h);
           if constexpr (NOB > 1) zemit_group<GP, WS1, Ring<zs_abs(S1)>>(w1, wring_a + R1, rn + zs_abs(S1) * (S1 > 0 ? lpp : lpm), h);
           if constexpr (NOB > 2) zemit_group<GP, WS2, Ring<zs_abs(S2)>>(w2, wring_a + R2, rn + zs_abs(S2) * (S2 > 0 ? lpp : lpm), h);
@@ -716,19 +770,8 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
         const int32_t i = fi0 + 8 * rn;
         ptx::red_global_add_if(frow + i, v, v != 0 && frow != nullptr && i >= 0 && i < fW);
       }
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (ZLAST) {   // the last of the NW warps to release stage k refills it
-          uint32_t old;
-          asm volatile("atom.shared.inc.u32 %0, [%1], %2;" : "=r"(old) : "r"(ptx::smem_addr(rel + k)), "r"((uint32_t)(NW - 1)) : "memory");
-          if (old == (uint32_t)(NW - 1)) issue_stage(k);
-        } else {
-          ptx::mbar_arrive_addr(bar_a + 8u * (uint32_t)(STAGES + k));
-        }
-      }
-      if (++k == STAGES) { k = 0; ph ^= 1u; }
-      if (lagc < ZLAG) ++lagc;
-      else if (++kl == STAGES) { kl = 0; phl ^= 1u; }
+      if constexpr (SPL == 1) release();
+      else __syncwarp();
       if (++pw == NW) pw = 0;
     };
     auto end_emit = [&]<int R>(const int rn_end) {
@@ -863,7 +906,7 @@ static int launch_zs(const dpm_volume_desc* d, const void* vox, const ImageSet& 
   const cuuint64_t dims[4] = {(cuuint64_t)d->L, (cuuint64_t)d->M, (cuuint64_t)d->N, (cuuint64_t)d->B};
   const cuuint64_t strides[3] = {(cuuint64_t)(d->stride_y * es), (cuuint64_t)(d->stride_z * es),
                                  (cuuint64_t)((d->B > 1 ? d->stride_b : d->stride_z * d->N) * es)};
-  const cuuint32_t box[4] = {(cuuint32_t)G::SX, (cuuint32_t)NW, 8, 1};
+  const cuuint32_t box[4] = {(cuuint32_t)G::SX, (cuuint32_t)NW, (cuuint32_t)(8 / zs_spl(K)), 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   const CUresult r = tensor_map_encoder()(&map, sizeof(T) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16,
                                           4, const_cast<void*>(vox), dims, strides, box, estr,
