@@ -269,6 +269,9 @@ int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+#ifndef DPM_M2_TARGET
+#define DPM_M2_TARGET 8    // row chunk: the longest that still gives this many CTAs per SM
+#endif
 #ifndef DPM_M2_MIN_RC
 #define DPM_M2_MIN_RC 16   // small images: shorter row chunks, more CTAs in flight (cfg1 graph 22.9 -> 18.8 us)
 #endif
@@ -276,7 +279,7 @@ int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_
   for (int64_t rc = 256; rc > DPM_M2_MIN_RC; rc >>= 1) {
     int64_t nb = 0;
     for (int k = 0; k < s.n_img; ++k) nb += ((s.W[k] + M2_THREADS - 1) / M2_THREADS) * ((s.H[k] + rc - 1) / rc);
-    if (nb * B >= 8 * (int64_t)sms) { p.rc = rc; break; }
+    if (nb * B >= DPM_M2_TARGET * (int64_t)sms) { p.rc = rc; break; }
   }
   p.blocks_img[0] = 0;
   for (int k = 0; k < s.n_img; ++k) {

@@ -178,9 +178,12 @@ template <> struct ZUnpack<uint16_t> {
     const uint32_t* w = reinterpret_cast<const uint32_t*>(&d);
     #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      if (DPM_ZS_UNPACK_FMA) {
+      if (DPM_ZS_UNPACK_FMA == 1) {
         asm("mul.hi.u32 %0, %1, %2;" : "=r"(v[2 * i + 1]) : "r"(w[i]), "r"(k16));
         v[2 * i] = ptx::mad_u32(v[2 * i + 1], 0u - k16, w[i]);
+      } else if (DPM_ZS_UNPACK_FMA == 2) {   // hi on the FMA pipe, lo on the ALU pipe
+        asm("mul.hi.u32 %0, %1, %2;" : "=r"(v[2 * i + 1]) : "r"(w[i]), "r"(k16));
+        asm("prmt.b32 %0, %1, 0, 0x4410;" : "=r"(v[2 * i]) : "r"(w[i]));
       } else {
         asm("prmt.b32 %0, %1, 0, 0x4410;" : "=r"(v[2 * i]) : "r"(w[i]));
         asm("prmt.b32 %0, %1, 0, 0x4432;" : "=r"(v[2 * i + 1]) : "r"(w[i]));
@@ -606,6 +609,13 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
     uint32_t* const frow = fj < NOB && yok ? p.img[DPM_IMG_DIAG + fj] + rowid * fW : nullptr;
     const int32_t fi0 = base_of(zs_form_s(fj)) + fk;
     uint32_t* const xyrow = lane < 8 && yok ? p.img[DPM_IMG_XY] + rowid * p.N + Zs + lane : nullptr;
+    // the steps whose flushed cell i = fi0 + 8 rn lies in [0, fW), and whose XY-slot
+    // plane z + lane < N: one unsigned compare per step instead of four
+    const int32_t frlo = fi0 >= 0 ? 0 : (7 - fi0) / 8;
+    const int32_t frhi = frow != nullptr && fW > fi0 ? (fW - fi0 + 7) / 8 : 0;
+    const uint32_t frange = frhi > frlo ? (uint32_t)(frhi - frlo) : 0u;
+    uint32_t* const fptr = frow != nullptr ? frow + fi0 : nullptr;
+    const int32_t xylim = xyrow != nullptr && p.N - Zs - lane > 0 ? (int32_t)((p.N - Zs - lane + 7) / 8) : 0;
     const int32_t pbase = base_of(SP);
     unsigned long long* const prow = p.prof + b * p.WQ;
 
@@ -759,7 +769,7 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
         __syncwarp();
         yzmine = lane < 8 ? ptx::lds_u32(ptx::smem_addr(xyv + (lane & 7))) : 0u;
       }
-      ptx::red_global_add_if(xyrow + 8 * rn, yzmine, xyrow != nullptr && z + lane < p.N && yzmine != 0);
+      ptx::red_global_add_if(xyrow + 8 * rn, yzmine, rn < xylim && yzmine != 0);
       __syncwarp();
       // the ring block this step completed: lanes 8j..8j+7 flush form j's 8 cells
       if (fj < NOB) {
@@ -767,8 +777,7 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
         const uint32_t a = fring_a + 4u * (uint32_t)((m & (fas - 1)) * 32 + (m >> (fas - 1)));
         const uint32_t v = ptx::lds_u32(a);
         ptx::sts_u32(a, 0u);
-        const int32_t i = fi0 + 8 * rn;
-        ptx::red_global_add_if(frow + i, v, v != 0 && frow != nullptr && i >= 0 && i < fW);
+        ptx::red_global_add_if(fptr + 8 * rn, v, v != 0 && (uint32_t)(rn - frlo) < frange);
       }
       if constexpr (SPL == 1) release();
       else __syncwarp();
