@@ -41,17 +41,6 @@ __device__ __forceinline__ void mbar_wait_addr(uint32_t bar, uint32_t phase) {
       : "memory");
 }
 
-// non-blocking: true iff the phase with parity `phase` of the barrier completed
-__device__ __forceinline__ bool mbar_test_addr(uint32_t bar, uint32_t phase) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok) : "r"(bar), "r"(phase) : "memory");
-  return ok != 0;
-}
-
 // the same with a suspend-time hint (ns): the warp sleeps until the phase
 // completes or the hint expires instead of re-polling (no issue slots spent)
 __device__ __forceinline__ void mbar_wait_addr_sleep(uint32_t bar, uint32_t phase, uint32_t hint_ns) {
