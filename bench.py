@@ -462,7 +462,7 @@ def main():
         "config": workload_config(cfg, world, cache_note(cfg)),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
-                     "kernel": "project_stream (projection stage incl. image zeroing)" if cfg == 5 else "whole pipeline",
+                     "kernel": "zstream_kernel (the layout-T projection pass alone; its buffers are re-zeroed by the moments stage)" if cfg == 5 else "whole pipeline (one graph replay)",
                      "traffic": tr},
         "cpu_baseline": cpu,
         "e2e": e2e,

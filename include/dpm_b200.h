@@ -170,6 +170,15 @@ DPM_API int dpm_moments_image_layout(const dpm_volume_desc* desc, int order, int
  * uint64).  Zeroes its outputs first. */
 DPM_API int dpm_project_profile(const dpm_volume_desc* desc, const void* d_voxels, int order,
                 uint32_t* const* d_images, uint64_t* d_profile, void* stream);
+/* The same two halves separately, for callers that keep the buffers and
+ * re-zero them right after their moments are taken (engine.GraphedSlabStages:
+ * the zeroing rides the moments stage, the projection stage is the pass alone):
+ * dpm_zero_profile_buffers zeroes the images and the profile (one launch),
+ * dpm_project_profile_zeroed runs the pass on buffers the caller zeroed. */
+DPM_API int dpm_zero_profile_buffers(const dpm_volume_desc* desc, int order, uint32_t* const* d_images,
+                uint64_t* d_profile, void* stream);
+DPM_API int dpm_project_profile_zeroed(const dpm_volume_desc* desc, const void* d_voxels, int order,
+                uint32_t* const* d_images, uint64_t* d_profile, void* stream);
 /* Exact moments of those images (2D) and of the profile (1D, into the q = 0
  * entries of slot DPM_IMG_ZX): a DPM_ACC_PROFILE accumulator, zeroed first. */
 DPM_API int dpm_moments2d_profile(const dpm_volume_desc* desc, int order, const uint32_t* const* d_images,

@@ -28,7 +28,8 @@ EXPORTS = (
     "dpm_project_workspace_bytes", "dpm_project", "dpm_moments2d", "dpm_derive3d",
     "dpm_workspace_bytes", "dpm_moments", "dpm_check_envelope", "dpm_acc_add",
     "dpm_synth_noise_u16", "dpm_last_launch_count", "dpm_strerror", "dpm_image_moments2d",
-    "dpm_project_generic", "dpm_profile_layout", "dpm_project_profile", "dpm_moments2d_profile",
+    "dpm_project_generic", "dpm_profile_layout", "dpm_project_profile", "dpm_zero_profile_buffers",
+    "dpm_project_profile_zeroed", "dpm_moments2d_profile",
     "dpm_partial_workspace_bytes", "dpm_moments_partial", "dpm_moments2d_profile_derive",
     "dpm_moments_acc_kind", "dpm_moments_image_layout", "dpm_direct_workspace_bytes", "dpm_direct_moments",
 )
@@ -78,6 +79,8 @@ def lib() -> ctypes.CDLL:
         "dpm_profile_layout": (ctypes.c_int, [pdesc, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64),
                                               ctypes.POINTER(ctypes.c_int)]),
         "dpm_project_profile": (ctypes.c_int, [pdesc, vp, ctypes.c_int, ctypes.POINTER(vp), vp, vp]),
+        "dpm_zero_profile_buffers": (ctypes.c_int, [pdesc, ctypes.c_int, ctypes.POINTER(vp), vp, vp]),
+        "dpm_project_profile_zeroed": (ctypes.c_int, [pdesc, vp, ctypes.c_int, ctypes.POINTER(vp), vp, vp]),
         "dpm_moments2d_profile": (ctypes.c_int, [pdesc, ctypes.c_int, ctypes.POINTER(vp), vp, vp, vp]),
         "dpm_moments2d_profile_derive": (ctypes.c_int, [pdesc, ctypes.c_int, ctypes.POINTER(vp), vp, vp, vp, vp, vp,
                                                          vp, vp]),

@@ -308,14 +308,9 @@ static int moments2d_profile_launch(const dpm_volume_desc* desc, int order, cons
   return launch_moments2d(s, desc->B, order, jb, d_acc, st, &ex);
 }
 
-int dpm_project_profile(const dpm_volume_desc* desc, const void* d_voxels, int order, uint32_t* const* d_images,
-                        uint64_t* d_profile, void* stream) {
-  reset_launches();
-  int rc = check_desc(desc);
-  if (rc) return rc;
-  if (check_order(order) || !d_images || !d_voxels || !d_profile) return DPM_EINVAL;
+static int zero_profile_buffers(const dpm_volume_desc* desc, int order, uint32_t* const* d_images,
+                                uint64_t* d_profile, cudaStream_t st) {
   const int n_img = num_images(order);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   ImageSet s = make_set(desc, n_img, d_images, true);
   ZeroList z;
   z.n = 0;
@@ -328,7 +323,37 @@ int dpm_project_profile(const dpm_volume_desc* desc, const void* d_voxels, int o
   const ProfGeom pg = profile_geom(desc, order);
   z.p[z.n] = reinterpret_cast<uint8_t*>(d_profile);
   z.bytes[z.n++] = (uint64_t)(pg.WQ * desc->B) * sizeof(uint64_t);
-  rc = zero_list_async(z, st);   // one launch; the projection kernel starts while it drains (PDL)
+  return zero_list_async(z, st);
+}
+
+int dpm_zero_profile_buffers(const dpm_volume_desc* desc, int order, uint32_t* const* d_images, uint64_t* d_profile,
+                             void* stream) {
+  reset_launches();
+  int rc = check_desc(desc);
+  if (rc) return rc;
+  if (check_order(order) || !d_images || !d_profile) return DPM_EINVAL;
+  return zero_profile_buffers(desc, order, d_images, d_profile, static_cast<cudaStream_t>(stream));
+}
+
+int dpm_project_profile_zeroed(const dpm_volume_desc* desc, const void* d_voxels, int order, uint32_t* const* d_images,
+                               uint64_t* d_profile, void* stream) {
+  reset_launches();
+  int rc = check_desc(desc);
+  if (rc) return rc;
+  if (check_order(order) || !d_images || !d_voxels || !d_profile) return DPM_EINVAL;
+  for (int k = 0; k < num_images(order); ++k)
+    if (k != DPM_IMG_ZX && !d_images[k]) return DPM_EINVAL;
+  return project_profile_launch(desc, d_voxels, order, d_images, d_profile, static_cast<cudaStream_t>(stream));
+}
+
+int dpm_project_profile(const dpm_volume_desc* desc, const void* d_voxels, int order, uint32_t* const* d_images,
+                        uint64_t* d_profile, void* stream) {
+  reset_launches();
+  int rc = check_desc(desc);
+  if (rc) return rc;
+  if (check_order(order) || !d_images || !d_voxels || !d_profile) return DPM_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  rc = zero_profile_buffers(desc, order, d_images, d_profile, st);   // the pass starts while it drains (PDL)
   if (rc) return rc;
   return project_profile_launch(desc, d_voxels, order, d_images, d_profile, st);
 }

@@ -274,10 +274,12 @@ def moments2d_partial(vox: torch.Tensor, order: int, offset: int = 0, z0: int = 
 
 def project_profile(vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0,
                     stream: torch.cuda.Stream | None = None, imgs: list[torch.Tensor | None] | None = None,
-                    profile: torch.Tensor | None = None) -> tuple[list[torch.Tensor | None], torch.Tensor]:
+                    profile: torch.Tensor | None = None,
+                    zeroed: bool = False) -> tuple[list[torch.Tensor | None], torch.Tensor]:
     """Projection pass of the moments pipeline: the order's images except ZX
     (slot 2 is None) as int32 [B, H, W] uint32 bits, and the y-summed profile
-    as int64 [B, WQ] (uint64 bits)."""
+    as int64 [B, WQ] (uint64 bits).  ``zeroed``: the caller's ``imgs`` and
+    ``profile`` are already zero (``zero_profile_buffers``); only the pass runs."""
     check_order(order)
     desc = make_desc(vox, offset, z0)
     n_img = num_images(order)
@@ -293,9 +295,23 @@ def project_profile(vox: torch.Tensor, order: int, offset: int = 0, z0: int = 0,
         wq, _, _ = profile_layout(desc, order)
         profile = torch.empty((desc.B, wq), dtype=torch.int64, device=vox.device)
     ptrs = (ctypes.c_void_p * n_img)(*[t.data_ptr() if t is not None else None for t in imgs])
-    nat.check(nat.lib().dpm_project_profile(ctypes.byref(desc), vox.data_ptr(), order, ptrs, profile.data_ptr(),
-                                            stream_handle(stream)), "dpm_project_profile")
+    if zeroed:
+        nat.check(nat.lib().dpm_project_profile_zeroed(ctypes.byref(desc), vox.data_ptr(), order, ptrs,
+                                                       profile.data_ptr(), stream_handle(stream)),
+                  "dpm_project_profile_zeroed")
+    else:
+        nat.check(nat.lib().dpm_project_profile(ctypes.byref(desc), vox.data_ptr(), order, ptrs, profile.data_ptr(),
+                                                stream_handle(stream)), "dpm_project_profile")
     return imgs, profile
+
+
+def zero_profile_buffers(vox: torch.Tensor, order: int, imgs: list[torch.Tensor | None], profile: torch.Tensor,
+                         offset: int = 0, z0: int = 0, stream: torch.cuda.Stream | None = None) -> None:
+    """Zero the moments pipeline's images and profile (one launch)."""
+    desc = make_desc(vox, offset, z0, validate=False)
+    ptrs = (ctypes.c_void_p * len(imgs))(*[t.data_ptr() if t is not None else None for t in imgs])
+    nat.check(nat.lib().dpm_zero_profile_buffers(ctypes.byref(desc), order, ptrs, profile.data_ptr(),
+                                                 stream_handle(stream)), "dpm_zero_profile_buffers")
 
 
 def moments2d_profile(vox: torch.Tensor, imgs: list[torch.Tensor | None], profile: torch.Tensor, order: int,
@@ -457,23 +473,39 @@ class GraphedSlabStages:
             f64=torch.empty((desc.B, n3d(order)), dtype=torch.float64, device=dev),
             status=torch.empty((desc.B,), dtype=torch.int32, device=dev), launches=0)
         self.counters = torch.empty((desc.B,), dtype=torch.int32, device=dev)
+        # The images and profile are zeroed once here and then by the moments
+        # stage right after it has read them (for the next step), so the
+        # projection stage is the pass alone.
         stages = [self._project, self._moments2d] + ([] if fused else [self._derive])
         st = torch.cuda.Stream(device=dev)
         st.wait_stream(torch.cuda.current_stream(dev))
         self.graphs, self.launches = [], 0
+        self._lc = 0
         with torch.cuda.stream(st):
+            self._zero()
             for fn in stages:                  # warm-up: attributes, tensor-map encoder
+                self._lc = 0
                 fn()
-                self.launches += nat.last_launch_count()
+                self.launches += self._lc
             for fn in stages:
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=st):
                     fn()
                 self.graphs.append(g)
+            self._zero_graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self._zero_graph, stream=st):
+                self._zero()
         torch.cuda.current_stream(dev).wait_stream(st)
+        self._dirty = False                    # images hold a projection not yet taken by the moments stage
+
+    def _zero(self):
+        zero_profile_buffers(self.vox, self.order, self.imgs, self.profile, self.offset, self.z0)
+        self._lc += nat.last_launch_count()
 
     def _project(self):
-        project_profile(self.vox, self.order, self.offset, self.z0, imgs=self.imgs, profile=self.profile)
+        project_profile(self.vox, self.order, self.offset, self.z0, imgs=self.imgs, profile=self.profile,
+                        zeroed=True)
+        self._lc += nat.last_launch_count()
 
     def _moments2d(self):
         if self.fused:
@@ -485,17 +517,24 @@ class GraphedSlabStages:
                 self.out.status.data_ptr(), stream_handle(None)), "dpm_moments2d_profile_derive")
         else:
             moments2d_profile(self.vox, self.imgs, self.profile, self.order, self.offset, self.z0, acc=self.acc)
+        self._lc += nat.last_launch_count()
+        self._zero()   # ready for the next projection
 
     def _derive(self):
         derive(self.acc, self.order, out=self.out, kind=self.kind)
+        self._lc += nat.last_launch_count()
 
     def replay_project(self) -> None:
+        if self._dirty:                        # a projection whose moments were never taken: start clean
+            self._zero_graph.replay()
         self.graphs[0].replay()
+        self._dirty = True
 
     def replay_moments2d(self) -> torch.Tensor:
         """Exact 2D moments into ``acc`` (with ``fused`` the epilogue already
         ran in the same launch: ``acc`` is then final, not for an exchange)."""
         self.graphs[1].replay()
+        self._dirty = False
         return self.acc
 
     def replay_derive(self) -> DeviceMoments:

@@ -212,3 +212,26 @@ def test_public_api_upload_is_thread_safe():
         got = list(ex.map(run, range(2)))
     for i in range(2):
         assert all(g == want[i] for g in got[i]), i
+
+
+def test_graphed_stages_rezero_between_steps():
+    """The moments stage re-zeroes the images and profile for the next step,
+    so the projection stage is the pass alone; a projection replayed twice
+    without its moments in between starts from zeroed buffers again."""
+    import oracle
+    rng = np.random.default_rng(17)
+    host = rng.integers(0, 65535, size=(40, 20, 264)).astype(np.uint16)
+    vol = torch.from_numpy(host).cuda()
+    want = oracle.dpm(host, 5)
+    idx = vm.moment_indices(5)
+    for fused in (False, True):
+        st = engine.GraphedSlabStages(vol, 5, fused=fused)
+        for rep in range(3):
+            st.replay_project()
+            if rep == 1:
+                st.replay_project()          # no moments in between: restarts clean
+            st.replay_moments2d()
+            res = st.replay_derive()
+            torch.cuda.synchronize()
+            assert int(res.status[0]) == 0
+            assert engine.i128_to_ints(res.i128[0].cpu().numpy()) == [want[k] for k in idx], (fused, rep)
