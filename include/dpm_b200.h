@@ -175,14 +175,6 @@ DPM_API int dpm_project_profile(const dpm_volume_desc* desc, const void* d_voxel
  * the zeroing rides the moments stage, the projection stage is the pass alone):
  * dpm_zero_profile_buffers zeroes the images and the profile (one launch),
  * dpm_project_profile_zeroed runs the pass on buffers the caller zeroed. */
-/* dpm_moments2d_profile (d_counters == NULL) or ..._derive (d_counters set)
- * with flags: DPM_M2_CLEAR makes the launch CONSUME its inputs -- every pixel
- * and profile cell is zeroed right after it is read, so the buffers are ready
- * for the next dpm_project_profile_zeroed without a separate zeroing pass. */
-#define DPM_M2_CLEAR 1
-DPM_API int dpm_moments2d_profile_ex(const dpm_volume_desc* desc, int order, uint32_t* const* d_images,
-                uint64_t* d_profile, uint64_t* d_acc, uint32_t* d_counters, int64_t* d_m3d_i128,
-                double* d_m3d_f64, int32_t* d_status, int flags, void* stream);
 DPM_API int dpm_zero_profile_buffers(const dpm_volume_desc* desc, int order, uint32_t* const* d_images,
                 uint64_t* d_profile, void* stream);
 DPM_API int dpm_project_profile_zeroed(const dpm_volume_desc* desc, const void* d_voxels, int order,

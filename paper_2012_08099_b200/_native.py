@@ -29,12 +29,11 @@ EXPORTS = (
     "dpm_workspace_bytes", "dpm_moments", "dpm_check_envelope", "dpm_acc_add",
     "dpm_synth_noise_u16", "dpm_last_launch_count", "dpm_strerror", "dpm_image_moments2d",
     "dpm_project_generic", "dpm_profile_layout", "dpm_project_profile", "dpm_zero_profile_buffers",
-    "dpm_project_profile_zeroed", "dpm_moments2d_profile", "dpm_moments2d_profile_ex",
+    "dpm_project_profile_zeroed", "dpm_moments2d_profile",
     "dpm_partial_workspace_bytes", "dpm_moments_partial", "dpm_moments2d_profile_derive",
     "dpm_moments_acc_kind", "dpm_moments_image_layout", "dpm_direct_workspace_bytes", "dpm_direct_moments",
 )
 DPM_DIRECT_NAIVE, DPM_DIRECT_FACTORED = 0, 1
-DPM_M2_CLEAR = 1   # dpm_moments2d_profile_ex flag: consume (zero) the images and profile
 
 
 class VolumeDesc(ctypes.Structure):
@@ -81,8 +80,6 @@ def lib() -> ctypes.CDLL:
                                               ctypes.POINTER(ctypes.c_int)]),
         "dpm_project_profile": (ctypes.c_int, [pdesc, vp, ctypes.c_int, ctypes.POINTER(vp), vp, vp]),
         "dpm_zero_profile_buffers": (ctypes.c_int, [pdesc, ctypes.c_int, ctypes.POINTER(vp), vp, vp]),
-        "dpm_moments2d_profile_ex": (ctypes.c_int, [pdesc, ctypes.c_int, ctypes.POINTER(vp), vp, vp, vp, vp, vp, vp,
-                                                    ctypes.c_int, vp]),
         "dpm_project_profile_zeroed": (ctypes.c_int, [pdesc, vp, ctypes.c_int, ctypes.POINTER(vp), vp, vp]),
         "dpm_moments2d_profile": (ctypes.c_int, [pdesc, ctypes.c_int, ctypes.POINTER(vp), vp, vp, vp]),
         "dpm_moments2d_profile_derive": (ctypes.c_int, [pdesc, ctypes.c_int, ctypes.POINTER(vp), vp, vp, vp, vp, vp,

@@ -290,14 +290,13 @@ static int project_profile_launch(const dpm_volume_desc* desc, const void* d_vox
 struct FusedOut { unsigned int* cnt; int64_t* i128; double* f64; int32_t* status; };
 static int moments2d_profile_launch(const dpm_volume_desc* desc, int order, const uint32_t* const* d_images,
                                     const uint64_t* d_profile, uint64_t* d_acc, cudaStream_t st,
-                                    const FusedOut* fused = nullptr, int clear = 0) {
+                                    const FusedOut* fused = nullptr) {
   const int n_img = num_images(order);
   ImageSet s = make_set(desc, n_img, const_cast<uint32_t* const*>(d_images), true);
   const int jb = jbits_for(desc, n_img, true);
   if (jb > 21) return DPM_EOVERFLOW;
   const ProfGeom pg = profile_geom(desc, order);
   M2Extra ex;
-  ex.clear = clear;
   ex.kind = acc_kind_of(desc);
   ex.prof = reinterpret_cast<const unsigned long long*>(d_profile);
   ex.WQ = pg.WQ;
@@ -396,38 +395,6 @@ int dpm_moments2d_profile_derive(const dpm_volume_desc* desc, int order, const u
   f.f64 = d_m3d_f64;
   f.status = d_status;
   return moments2d_profile_launch(desc, order, d_images, d_profile, d_acc, st, &f);
-}
-
-int dpm_moments2d_profile_ex(const dpm_volume_desc* desc, int order, uint32_t* const* d_images, uint64_t* d_profile,
-                             uint64_t* d_acc, uint32_t* d_counters, int64_t* d_m3d_i128, double* d_m3d_f64,
-                             int32_t* d_status, int flags, void* stream) {
-  reset_launches();
-  int rc = check_desc(desc);
-  if (rc) return rc;
-  if (check_order(order) || !d_images || !d_profile || !d_acc) return DPM_EINVAL;
-  const bool fused = d_counters != nullptr;
-  if (fused && (!d_m3d_i128 || !d_status)) return DPM_EINVAL;
-  if (flags & ~DPM_M2_CLEAR) return DPM_EINVAL;
-  const int n_img = num_images(order);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  ZeroList z;
-  z.n = 1;
-  z.p[0] = reinterpret_cast<uint8_t*>(d_acc);
-  z.bytes[0] = (uint64_t)(desc->B * n_img * n2d(order) * 4) * sizeof(uint64_t);
-  if (fused) {
-    z.p[1] = reinterpret_cast<uint8_t*>(d_counters);
-    z.bytes[1] = (uint64_t)desc->B * sizeof(uint32_t);
-    z.n = 2;
-  }
-  rc = zero_list_async(z, st);
-  if (rc) return rc;
-  FusedOut f;
-  f.cnt = d_counters;
-  f.i128 = d_m3d_i128;
-  f.f64 = d_m3d_f64;
-  f.status = d_status;
-  return moments2d_profile_launch(desc, order, d_images, d_profile, d_acc, st, fused ? &f : nullptr,
-                                  (flags & DPM_M2_CLEAR) ? 1 : 0);
 }
 
 size_t dpm_partial_workspace_bytes(const dpm_volume_desc* desc, int order) {

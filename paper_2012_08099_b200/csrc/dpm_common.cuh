@@ -63,7 +63,6 @@ template <> struct VoxelTraits<int16_t>  { static __device__ __forceinline__ uin
 // profile's 1D moments in the same grid, and the fused epilogue (the last
 // block of each volume runs derive_volume; cnt[B] zeroed by the caller).
 struct M2Extra {
-  int clear;                // zero every pixel and profile cell right after reading it
   const unsigned long long* prof;
   int64_t WQ, ai;
   int kind;                 // accumulator kind of the fused epilogue (DPM_ACC_PROFILE / _T)

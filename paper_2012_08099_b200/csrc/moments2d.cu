@@ -43,7 +43,6 @@ struct M2Params {
   // moments pipeline: the profile's 1D moments in the same launch (pblocks
   // extra blocks per volume, into the q = 0 entries of slot DPM_IMG_ZX)
   const unsigned long long* prof;          // [B][WQ] or null
-  int clear;                               // consume: zero each pixel / profile cell after reading it
   int64_t WQ, prof_ai, pblocks;
   // fused epilogue: the last block of each volume (counter cnt[b], zeroed by
   // the caller) runs derive_volume for it; null out_i128 = separate derive3d
@@ -63,7 +62,6 @@ __device__ __forceinline__ void profile_block(const M2Params& p, int64_t b, int6
   for (int a = 0; a <= K; ++a) { l[a][0] = l[a][1] = l[a][2] = l[a][3] = 0; }
   for (int64_t i = chunk * M2_THREADS + tid; i < p.WQ; i += p.pblocks * M2_THREADS) {
     const unsigned long long v = p.prof[b * p.WQ + i];
-    if (p.clear) const_cast<unsigned long long*>(p.prof)[b * p.WQ + i] = 0ull;
     if (v == 0) continue;
     const __int128 x = (__int128)(i + p.prof_ai);
     __int128 pw = 1;
@@ -147,16 +145,10 @@ __global__ void DPM_M2_BOUNDS moments2d_kernel(M2Params p) {
   #pragma unroll
   for (int l = 0; l < NTP; ++l) acc[l] = 0;
   if (i < W) {
-    uint32_t* col = p.s.img[k] + b * W * H + j0 * W + i;
+    const uint32_t* col = p.s.img[k] + b * W * H + j0 * W + i;
     #pragma unroll M2_UNROLL
     for (int rr = 0; rr < rows; ++rr) {
-      uint64_t v;
-      if (p.clear) {   // consume: the buffers are zero for the next projection (no separate zeroing pass)
-        v = __ldcs(col + (int64_t)rr * W);
-        __stcs(col + (int64_t)rr * W, 0u);
-      } else {
-        v = __ldg(col + (int64_t)rr * W);
-      }
+      const uint64_t v = __ldg(col + (int64_t)rr * W);
       const uint4* tr = reinterpret_cast<const uint4*>(&table[rr][0]);
       #pragma unroll
       for (int l4 = 0; l4 < NTP / 4; ++l4) {
@@ -265,7 +257,6 @@ int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_
   M2Params p;
   p.s = s; p.B = B; p.acc = acc;
   p.prof = ex ? ex->prof : nullptr;
-  p.clear = ex ? ex->clear : 0;
   p.WQ = ex ? ex->WQ : 0;
   p.prof_ai = ex ? ex->ai : 0;
   p.pblocks = p.prof ? imin64((p.WQ + M2_THREADS - 1) / M2_THREADS, 16) : 0;

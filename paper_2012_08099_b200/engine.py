@@ -328,25 +328,6 @@ def moments2d_profile(vox: torch.Tensor, imgs: list[torch.Tensor | None], profil
     return acc
 
 
-def moments2d_profile_consume(vox: torch.Tensor, imgs: list[torch.Tensor | None], profile: torch.Tensor,
-                              order: int, acc: torch.Tensor, offset: int = 0, z0: int = 0,
-                              counters: torch.Tensor | None = None, out: "DeviceMoments | None" = None,
-                              stream: torch.cuda.Stream | None = None) -> torch.Tensor:
-    """``moments2d_profile`` that CONSUMES its inputs: every pixel and profile
-    cell is zeroed right after it is read (``DPM_M2_CLEAR``), leaving the buffers
-    ready for ``project_profile(..., zeroed=True)``.  With ``counters`` and
-    ``out`` the same launch ends with the epilogue (single device)."""
-    desc = make_desc(vox, offset, z0, validate=False)
-    ptrs = (ctypes.c_void_p * len(imgs))(*[t.data_ptr() if t is not None else None for t in imgs])
-    fused = counters is not None
-    nat.check(nat.lib().dpm_moments2d_profile_ex(
-        ctypes.byref(desc), order, ptrs, profile.data_ptr(), acc.data_ptr(),
-        counters.data_ptr() if fused else None, out.i128.data_ptr() if fused else None,
-        out.f64.data_ptr() if fused else None, out.status.data_ptr() if fused else None,
-        nat.DPM_M2_CLEAR, stream_handle(stream)), "dpm_moments2d_profile_ex")
-    return acc
-
-
 ACC_KINDS = {"profile": nat.DPM_ACC_PROFILE, "profile_t": nat.DPM_ACC_PROFILE_T, "images": nat.DPM_ACC_IMAGES}
 
 
@@ -527,11 +508,17 @@ class GraphedSlabStages:
         self._lc += nat.last_launch_count()
 
     def _moments2d(self):
-        # consumes the images and profile: zeroed as they are read, ready for the next projection
-        moments2d_profile_consume(self.vox, self.imgs, self.profile, self.order, self.acc, self.offset, self.z0,
-                                  counters=self.counters if self.fused else None,
-                                  out=self.out if self.fused else None)
+        if self.fused:
+            desc = make_desc(self.vox, self.offset, self.z0, validate=False)
+            ptrs = (ctypes.c_void_p * len(self.imgs))(*[t.data_ptr() if t is not None else None for t in self.imgs])
+            nat.check(nat.lib().dpm_moments2d_profile_derive(
+                ctypes.byref(desc), self.order, ptrs, self.profile.data_ptr(), self.acc.data_ptr(),
+                self.counters.data_ptr(), self.out.i128.data_ptr(), self.out.f64.data_ptr(),
+                self.out.status.data_ptr(), stream_handle(None)), "dpm_moments2d_profile_derive")
+        else:
+            moments2d_profile(self.vox, self.imgs, self.profile, self.order, self.offset, self.z0, acc=self.acc)
         self._lc += nat.last_launch_count()
+        self._zero()   # ready for the next projection
 
     def _derive(self):
         derive(self.acc, self.order, out=self.out, kind=self.kind)

@@ -114,4 +114,4 @@ def test_graphed_slab_stages(cuda, order):
         res = st.replay_derive()
         torch.cuda.synchronize()
         assert torch.equal(res.i128, engine.derive(want_acc, order, kind=engine.acc_kind(slab, order)).i128)
-    assert st.launches == 4   # projection, accumulator zeroing + moments (consuming the images), epilogue
+    assert st.launches == 5   # zeroing + projection, zeroing + image/profile moments, epilogue

@@ -124,7 +124,7 @@ def test_profile_graphed_stages_launches():
     rng = np.random.default_rng(2)
     slab = torch.from_numpy(rng.integers(0, 65535, size=(24, 24, 264)).astype(np.uint16)).cuda()
     st = engine.GraphedSlabStages(slab, 6, z0=16)
-    assert st.launches == 4      # projection, accumulator zeroing + moments (consuming the images), epilogue
+    assert st.launches == 5      # zeroing + projection, zeroing + image/profile moments (one launch), epilogue
 
 
 @pytest.mark.parametrize("order", [4, 6])
@@ -186,7 +186,7 @@ def test_graphed_slab_stages_fused_epilogue(order):
     vol = torch.from_numpy(rng.integers(0, 65535, size=(120, 30, 264)).astype(np.uint16)).cuda()
     sep = engine.GraphedSlabStages(vol, order, z0=5)
     fused = engine.GraphedSlabStages(vol, order, z0=5, fused=True)
-    assert fused.launches == 3   # projection, accumulator zeroing + moments with the epilogue
+    assert fused.launches == 4   # zeroing + projection, zeroing + moments with the epilogue
     for _ in range(2):
         sep.replay_project(); sep.replay_moments2d(); a = sep.replay_derive()
         fused.replay_project(); fused.replay_moments2d(); b = fused.replay_derive()
