@@ -186,6 +186,29 @@ def test_cfg5_full_volume_exact(cuda):
     assert want[(0, 0, 0)] == int(host.sum(dtype=np.uint64))
 
 
+def test_cfg5_full_size_projection_rows_bit_exact(cuda):
+    """Projection verify mode at full size: the headline pass's
+    images of the 2048^3 volume -- the layout-T image set the moments pipeline
+    builds (engine.project_profile) -- compared bit for bit with the oracle's
+    projection of the x/z-exchanged volume, on image rows y in 0-7, 1024-1031
+    and 2040-2047 (every image except the y-summed profile is per row y; YZ is
+    stored [x][y], so those rows are its columns)."""
+    vol = engine.synth_noise(2048, 2048, 0, 2048, 5)
+    assert engine.acc_kind(vol, 6) == "profile_t"
+    imgs, _ = engine.project_profile(vol, 6)
+    torch.cuda.synchronize()
+    ys = np.r_[0:8, 1024:1032, 2040:2048]
+    sub = np.concatenate([vol[:, a:a + 8, :].cpu().numpy() for a in (0, 1024, 2040)], axis=1)   # (z, y, x) rows ys
+    transposed = np.ascontiguousarray(sub.transpose(2, 1, 0))           # V'(x', y, z') = V(z', y, x')
+    oracle.set_threads(oracle.max_threads())
+    want = oracle.project(transposed, 7)
+    for k in (0, 3, 4, 5, 6):                                           # [y][...] images
+        got = imgs[k][0][torch.from_numpy(ys).cuda()].cpu().numpy().view(np.uint32).astype(np.int64)
+        assert np.array_equal(got, want[k]), k
+    got_yz = imgs[1][0][:, torch.from_numpy(ys).cuda()].cpu().numpy().view(np.uint32).astype(np.int64)
+    assert np.array_equal(got_yz, want[1])
+
+
 @pytest.mark.parametrize("order", [3, 4, 5, 6])
 def test_derive_exactness_and_nonexact_flag(cuda, order):
     """Epilogue alone: exact results from a volume's limb accumulator (two
