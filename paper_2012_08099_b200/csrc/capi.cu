@@ -19,7 +19,8 @@ void reset_launches() { g_launches = 0; }
 int launch_project_generic(const dpm_volume_desc* d, const void* vox, const ImageSet& s, unsigned long long* prof,
                            cudaStream_t st, bool transposed = false);
 int launch_project_zstream(const dpm_volume_desc* d, const void* vox, int order, const ImageSet& s,
-                           unsigned long long* prof, int64_t WQ, cudaStream_t st, bool* handled);
+                           unsigned long long* prof, int64_t WQ, cudaStream_t st, bool* handled,
+                           bool signed_i16 = false);
 bool zstream_eligible(const dpm_volume_desc* d, const void* vox);
 bool fused_batch_eligible(const dpm_volume_desc* d, const void* vox, int order);
 int launch_fused_batch(const dpm_volume_desc* d, const void* vox, int order, uint64_t* acc, unsigned int* cnt,
@@ -98,6 +99,10 @@ int zero_async(void* p, size_t bytes, cudaStream_t st) {
   z.bytes[0] = bytes;
   return zero_list_async(z, st);
 }
+
+#ifndef DPM_SIGNED_I16
+#define DPM_SIGNED_I16 1
+#endif
 
 static int check_order(int order) { return (order >= 3 && order <= DPM_MAX_ORDER) ? DPM_OK : DPM_EINVAL; }
 
@@ -263,12 +268,13 @@ int dpm_profile_layout(const dpm_volume_desc* desc, int order, int64_t* WQ, int6
 // kernel stores complete rows -- zero them here if it declines)
 static int project_profile_launch(const dpm_volume_desc* desc, const void* d_voxels, int order,
                                   uint32_t* const* d_images, uint64_t* d_profile, cudaStream_t st,
-                                  bool images_zeroed = true) {
+                                  bool images_zeroed = true, bool signed_i16 = false) {
   ImageSet s = make_set(desc, num_images(order), d_images, true);
   unsigned long long* prof = reinterpret_cast<unsigned long long*>(d_profile);
   bool handled = false;
   if (layout_t(desc)) {
-    const int rc = launch_project_zstream(desc, d_voxels, order, s, prof, profile_geom(desc, order).WQ, st, &handled);
+    const int rc = launch_project_zstream(desc, d_voxels, order, s, prof, profile_geom(desc, order).WQ, st, &handled,
+                                          signed_i16);
     if (rc || handled) return rc;
     // shapes the z-streaming kernel cannot read (unaligned rows): the generic
     // brick kernel on the transposed view builds the same layout-T images
@@ -290,13 +296,16 @@ static int project_profile_launch(const dpm_volume_desc* desc, const void* d_vox
 struct FusedOut { unsigned int* cnt; int64_t* i128; double* f64; int32_t* status; };
 static int moments2d_profile_launch(const dpm_volume_desc* desc, int order, const uint32_t* const* d_images,
                                     const uint64_t* d_profile, uint64_t* d_acc, cudaStream_t st,
-                                    const FusedOut* fused = nullptr) {
+                                    const FusedOut* fused = nullptr, bool signed_i16 = false) {
   const int n_img = num_images(order);
   ImageSet s = make_set(desc, n_img, const_cast<uint32_t* const*>(d_images), true);
   const int jb = jbits_for(desc, n_img, true);
   if (jb > 21) return DPM_EOVERFLOW;
   const ProfGeom pg = profile_geom(desc, order);
   M2Extra ex;
+  ex.sgn = signed_i16 ? 1 : 0;
+  ex.off = desc->offset;
+  ex.L = desc->L; ex.M = desc->M; ex.N = desc->N;
   ex.kind = acc_kind_of(desc);
   ex.prof = reinterpret_cast<const unsigned long long*>(d_profile);
   ex.WQ = pg.WQ;
@@ -436,9 +445,15 @@ static int moments_partial_impl(const dpm_volume_desc* desc, const void* d_voxel
     return DPM_ECUDA;
   rc = zero_async(z0, zb, st);   // last before the projection kernel: it starts while this drains (PDL)
   if (rc) return rc;
-  rc = project_profile_launch(desc, d_voxels, order, imgs, prof, st, !single);
+  // signed-exact int16 (whole volumes through dpm_moments, layout T): the pass
+  // sums the raw signed voxels -- no per-voxel offset add, the 16-bit unpack costs
+  // what uint16's does -- and the epilogue adds offset x the box's moments
+  // (derive_volume's OffsetBox), exactly
+  const bool sgn = fused && desc->dtype == DPM_I16 && desc->offset != 0 && desc->z0 == 0 && layout_t(desc) &&
+                   zstream_eligible(desc, d_voxels) && DPM_SIGNED_I16;
+  rc = project_profile_launch(desc, d_voxels, order, imgs, prof, st, !single, sgn);
   if (rc) return rc;
-  return moments2d_profile_launch(desc, order, imgs, prof, d_acc, st, fused);
+  return moments2d_profile_launch(desc, order, imgs, prof, d_acc, st, fused, sgn);
 }
 
 int dpm_moments_partial(const dpm_volume_desc* desc, const void* d_voxels, int order, void* d_ws, size_t ws_bytes,

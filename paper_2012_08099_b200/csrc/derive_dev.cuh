@@ -88,9 +88,20 @@ __device__ __forceinline__ int64_t binom(int n, int k) {
 // words; `sst` = a shared status word.  All threads of the CTA call it.
 // `coherent`: read `a` through L2 (written by other CTAs' atomics in the same
 // grid, the fused tail of moments2d).
+// Signed-exact int16 (capi.cu): the pass summed the raw signed voxels; the
+// offset's share of every moment is off * S_P(L) S_Q(M) S_R(N) (power sums
+// S_e(n) = sum_{k < n} k^e of the box), added at placement in true (x, y, z) order.
+// off * S_e(L), S_e(M), S_e(N) (e = 0..6) as (lo, hi) int64 pairs, formed on
+// the host (capi.cu offset_box) so the epilogue only multiplies
+struct OffsetBox { int64_t s[3][DPM_MAX_ORDER + 1][2]; };
+__device__ __forceinline__ i128 box_sum(const OffsetBox& bx, int axis, int e) {
+  return (i128)(((unsigned __int128)(uint64_t)bx.s[axis][e][1] << 64) | (uint64_t)bx.s[axis][e][0]);
+}
+
 template <int K>
 __device__ void derive_volume(const uint64_t* a, int64_t b, int n_img, int kind, int64_t* out_i128, double* out_f64,
-                              int32_t* status, uint64_t* sa, int32_t* sst_p, bool coherent) {
+                              int32_t* status, uint64_t* sa, int32_t* sst_p, bool coherent,
+                              const OffsetBox* box = nullptr) {
   // DPM_ACC_PROFILE_T: the accumulator holds the layout-T image set (the volume
   // with x and z exchanged); the solve yields M'_pqr = M_rqp, stored relabelled
   const bool prof = kind == DPM_ACC_PROFILE || kind == DPM_ACC_PROFILE_T;
@@ -109,6 +120,10 @@ __device__ void derive_volume(const uint64_t* a, int64_t b, int n_img, int kind,
   auto m2 = [&](int img, int p, int q) -> i128 { return acc_to_i128(sa + (img * N2 + idx2(K, p, q)) * 4); };
   auto put = [&](int p, int q, int r, i128 v) {
     const int i = tr ? idx3(K, r, q, p) : idx3(K, p, q, r);
+    if (box) {   // true (x, y, z) exponents; the offset is folded into the x sums
+      const int P = tr ? r : p, R = tr ? p : r;
+      v += box_sum(*box, 0, P) * box_sum(*box, 1, q) * box_sum(*box, 2, R);
+    }
     const unsigned __int128 u = (unsigned __int128)v;
     out_i128[(b * N3 + i) * 2 + 0] = (int64_t)(uint64_t)u;
     out_i128[(b * N3 + i) * 2 + 1] = (int64_t)(uint64_t)(u >> 64);

@@ -63,6 +63,10 @@ template <> struct VoxelTraits<int16_t>  { static __device__ __forceinline__ uin
 // profile's 1D moments in the same grid, and the fused epilogue (the last
 // block of each volume runs derive_volume; cnt[B] zeroed by the caller).
 struct M2Extra {
+  // signed-exact int16: pixels are int32 (two's complement sums), the profile
+  // int64, and the epilogue adds off * (the box's moments); off = 0: plain
+  int sgn;
+  int64_t off, L, M, N;
   const unsigned long long* prof;
   int64_t WQ, ai;
   int kind;                 // accumulator kind of the fused epilogue (DPM_ACC_PROFILE / _T)

@@ -43,6 +43,8 @@ struct M2Params {
   // moments pipeline: the profile's 1D moments in the same launch (pblocks
   // extra blocks per volume, into the q = 0 entries of slot DPM_IMG_ZX)
   const unsigned long long* prof;          // [B][WQ] or null
+  int sgn;                                 // signed-exact int16: int32 pixels, int64 profile cells
+  OffsetBox box;                           // offset x box moments added by the epilogue (sgn only)
   int64_t WQ, prof_ai, pblocks;
   // fused epilogue: the last block of each volume (counter cnt[b], zeroed by
   // the caller) runs derive_volume for it; null out_i128 = separate derive3d
@@ -65,9 +67,11 @@ __device__ __forceinline__ void profile_block(const M2Params& p, int64_t b, int6
     if (v == 0) continue;
     const __int128 x = (__int128)(i + p.prof_ai);
     __int128 pw = 1;
+    // signed cells (sgn): the uint64 is a two's-complement int64
+    const unsigned __int128 vv = p.sgn ? (unsigned __int128)(__int128)(long long)v : (unsigned __int128)v;
     #pragma unroll
     for (int a = 0; a <= K; ++a) {
-      const unsigned __int128 t = (unsigned __int128)v * (unsigned __int128)pw;
+      const unsigned __int128 t = vv * (unsigned __int128)pw;
       l[a][0] += (uint32_t)t;
       l[a][1] += (uint32_t)(t >> 32);
       l[a][2] += (uint32_t)(t >> 64);
@@ -148,7 +152,9 @@ __global__ void DPM_M2_BOUNDS moments2d_kernel(M2Params p) {
     const uint32_t* col = p.s.img[k] + b * W * H + j0 * W + i;
     #pragma unroll M2_UNROLL
     for (int rr = 0; rr < rows; ++rr) {
-      const uint64_t v = __ldg(col + (int64_t)rr * W);
+      const uint32_t raw = __ldg(col + (int64_t)rr * W);
+      // signed pixels (sgn): sign-extended; the limb sums stay exact int64 (|v t| < 2^55, 256 rows)
+      const uint64_t v = p.sgn ? (uint64_t)(int64_t)(int32_t)raw : (uint64_t)raw;
       const uint4* tr = reinterpret_cast<const uint4*>(&table[rr][0]);
       #pragma unroll
       for (int l4 = 0; l4 < NTP / 4; ++l4) {
@@ -170,7 +176,9 @@ __global__ void DPM_M2_BOUNDS moments2d_kernel(M2Params p) {
   for (int q = 0; q <= K; ++q) {
     unsigned __int128 c = 0;
     #pragma unroll
-    for (int l = 0; l < LP::nl(q); ++l) c += ((unsigned __int128)acc[LP::off(q) + l]) << (24 * l);
+    for (int l = 0; l < LP::nl(q); ++l)
+      c += (p.sgn ? (unsigned __int128)(__int128)(int64_t)acc[LP::off(q) + l] : (unsigned __int128)acc[LP::off(q) + l])
+           << (24 * l);
     C[q] = (i < W) ? c : 0;
   }
   unsigned __int128 xp[K + 1];
@@ -227,7 +235,7 @@ __global__ void DPM_M2_BOUNDS moments2d_kernel(M2Params p) {
     if (last) {
       __threadfence();
       derive_volume<K>(p.acc + b * p.s.n_img * N2 * 4, b, p.s.n_img, p.kind, p.out_i128, p.out_f64,
-                       p.status, reinterpret_cast<uint64_t*>(m2_smem), &sst, true);
+                       p.status, reinterpret_cast<uint64_t*>(m2_smem), &sst, true, p.sgn ? &p.box : nullptr);
     }
   }
 }
@@ -252,11 +260,40 @@ static int launch_k(int jb, dim3 grid, cudaStream_t st, const M2Params& p) {
   return launch_kj<K, 21>(grid, st, p);
 }
 
+// off * S_e(L), S_e(M), S_e(N), S_e(n) = sum_{k < n} k^e, summed directly mod
+// 2^128 (no division, so exact in the ring the epilogue works in; the true
+// moments are below 2^126).  The last box is cached per thread: graph capture
+// and repeated calls on one geometry pay the O(L + M + N) loop once.
+static OffsetBox offset_box(int64_t off, int64_t L, int64_t M, int64_t N) {
+  thread_local int64_t key[4] = {-1, -1, -1, -1};
+  thread_local OffsetBox cached;
+  if (key[0] == off && key[1] == L && key[2] == M && key[3] == N) return cached;
+  OffsetBox bx;
+  const int64_t dims[3] = {L, M, N};
+  for (int a = 0; a < 3; ++a) {
+    unsigned __int128 S[DPM_MAX_ORDER + 1] = {};
+    for (int64_t k = 0; k < dims[a]; ++k) {
+      unsigned __int128 pw = 1;
+      for (int e = 0; e <= DPM_MAX_ORDER; ++e) { S[e] += pw; pw *= (unsigned __int128)k; }
+    }
+    for (int e = 0; e <= DPM_MAX_ORDER; ++e) {
+      const unsigned __int128 v = a == 0 ? S[e] * (unsigned __int128)(__int128)off : S[e];
+      bx.s[a][e][0] = (int64_t)(uint64_t)v;
+      bx.s[a][e][1] = (int64_t)(uint64_t)(v >> 64);
+    }
+  }
+  key[0] = off; key[1] = L; key[2] = M; key[3] = N;
+  cached = bx;
+  return bx;
+}
+
 int launch_moments2d(const ImageSet& s, int64_t B, int order, int jbits, uint64_t* acc, cudaStream_t st,
                      const M2Extra* ex) {
   M2Params p;
   p.s = s; p.B = B; p.acc = acc;
   p.prof = ex ? ex->prof : nullptr;
+  p.sgn = ex ? ex->sgn : 0;
+  if (p.sgn) p.box = offset_box(ex->off, ex->L, ex->M, ex->N);
   p.WQ = ex ? ex->WQ : 0;
   p.prof_ai = ex ? ex->ai : 0;
   p.pblocks = p.prof ? imin64((p.WQ + M2_THREADS - 1) / M2_THREADS, 16) : 0;

@@ -158,8 +158,21 @@ template <typename T, int K, int NW, int VX, int STAGES> struct ZGeo {
 };
 
 // ---- lane vectors ------------------------------------------------------------
+// s16: int16 voxels summed SIGNED, without the offset (dpm_moments adds
+// offset x the box's moments to the 3D moments exactly; capi.cu "signed-exact
+// int16"): cells hold two's-complement sums mod 2^32, the profile is sign-extended
+struct s16 { int16_t v; };
+template <typename T> struct ZSigned { static constexpr bool value = false; };
+template <> struct ZSigned<s16> { static constexpr bool value = true; };
+// a shared-memory u32 cell as the uint64 the profile atomics add
+template <typename T> __device__ __forceinline__ unsigned long long zprof64(uint32_t v) {
+  if constexpr (ZSigned<T>::value) return (unsigned long long)(long long)(int32_t)v;
+  else return (unsigned long long)v;
+}
+
 template <typename T, int VX> struct ZVec;
 template <> struct ZVec<uint16_t, 8> { using type = uint4; };
+template <> struct ZVec<s16, 8>      { using type = uint4; };
 template <> struct ZVec<int16_t, 8>  { using type = uint4; };
 template <> struct ZVec<uint8_t, 8>  { using type = uint2; };
 
@@ -200,6 +213,16 @@ template <> struct ZUnpack<int16_t> {   // sign-extend, add the offset (0 for ze
       asm("prmt.b32 %0, %1, 0, 0x9910;" : "=r"(lo) : "r"(w[i]));
       v[2 * i] = lo + (uint32_t)off;
       v[2 * i + 1] = (uint32_t)((int32_t)w[i] >> 16) + (uint32_t)off;
+    }
+  }
+};
+template <> struct ZUnpack<s16> {   // sign-extend only: PRMT (sign-replicate) + arithmetic shift
+  template <typename V> __device__ __forceinline__ static void run(const V& d, uint32_t* v, int32_t, uint32_t) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(&d);
+    #pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      asm("prmt.b32 %0, %1, 0, 0x9910;" : "=r"(v[2 * i]) : "r"(w[i]));
+      v[2 * i + 1] = (uint32_t)((int32_t)w[i] >> 16);
     }
   }
 };
@@ -663,7 +686,7 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
         const uint32_t v = ptx::lds_u32(a);
         ptx::sts_u32(a, 0u);
         const int32_t i = pbase + 8 * blk + lane;
-        if (v != 0 && i >= 0 && i < p.WQ) atomicAdd(prow + i, (unsigned long long)v);
+        if (v != 0 && i >= 0 && i < p.WQ) atomicAdd(prow + i, zprof64<T>(v));
       }
     };
     auto release = [&]() {   // this warp is done with (sub-)stage k
@@ -717,7 +740,9 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
             // byte / halfword dot products with ones on the FMA pipe, straight
             // from the packed words (the ALU pipe carries the folds)
             const uint32_t* wd = reinterpret_cast<const uint32_t*>(&draw[gg]);
-            if constexpr (sizeof(T) == 2) sm = __dp2a_lo(wd[0], 0x0101u, __dp2a_lo(wd[1], 0x0101u, __dp2a_lo(wd[2], 0x0101u, __dp2a_lo(wd[3], 0x0101u, 0u))));
+            if constexpr (ZSigned<T>::value)   // signed halves (sum mod 2^32 == the u32 cell arithmetic)
+              sm = (uint32_t)__dp2a_lo((int)wd[0], 0x0101, __dp2a_lo((int)wd[1], 0x0101, __dp2a_lo((int)wd[2], 0x0101, __dp2a_lo((int)wd[3], 0x0101, 0))));
+            else if constexpr (sizeof(T) == 2) sm = __dp2a_lo(wd[0], 0x0101u, __dp2a_lo(wd[1], 0x0101u, __dp2a_lo(wd[2], 0x0101u, __dp2a_lo(wd[3], 0x0101u, 0u))));
             else sm = __dp4a(wd[0], 0x01010101u, __dp4a(wd[1], 0x01010101u, 0u));
           } else if constexpr (VX == 8) {
             sm = (P[gg][0] + P[gg][1] + P[gg][2]) + (P[gg][3] + P[gg][4]) + (P[gg][5] + P[gg][6]) + P[gg][7];
@@ -860,7 +885,7 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
         const uint32_t v = ptx::lds_u32(a);
         ptx::sts_u32(a, 0u);
         const int32_t i = pbase + 8 * blk + kk;
-        if (v != 0 && i >= 0 && i < p.WQ) atomicAdd(prow + i, (unsigned long long)v);
+        if (v != 0 && i >= 0 && i < p.WQ) atomicAdd(prow + i, zprof64<T>(v));
       }
     }
     if (lane == 0) segs[w].next(p);
@@ -976,7 +1001,7 @@ static int launch_zs_k(int order, const dpm_volume_desc* d, const void* vox, con
 
 // layout-T moments projection pass; the caller zeroed the images and profile
 int launch_project_zstream(const dpm_volume_desc* d, const void* vox, int order, const ImageSet& s,
-                           unsigned long long* prof, int64_t WQ, cudaStream_t st, bool* handled) {
+                           unsigned long long* prof, int64_t WQ, cudaStream_t st, bool* handled, bool signed_i16) {
   *handled = false;
   if (!zstream_eligible(d, vox)) return DPM_OK;
   int dev = 0, sms = 148;
@@ -986,7 +1011,10 @@ int launch_project_zstream(const dpm_volume_desc* d, const void* vox, int order,
   switch (d->dtype) {
     case DPM_U8: rc = launch_zs_k<uint8_t>(order, d, vox, s, prof, WQ, sms, st); break;
     case DPM_U16: rc = launch_zs_k<uint16_t>(order, d, vox, s, prof, WQ, sms, st); break;
-    default: rc = launch_zs_k<int16_t>(order, d, vox, s, prof, WQ, sms, st); break;
+    default:
+      rc = signed_i16 ? launch_zs_k<s16>(order, d, vox, s, prof, WQ, sms, st)
+                      : launch_zs_k<int16_t>(order, d, vox, s, prof, WQ, sms, st);
+      break;
   }
   if (rc < 0) return DPM_OK;
   if (rc) return rc;

@@ -122,3 +122,25 @@ def test_layout_t_full_size_slab_schedule():
     oracle.set_threads(oracle.max_threads())
     want = oracle.dpm(vol.cpu().numpy(), 6)
     assert dict(zip(vm.moment_indices(6), engine.i128_to_ints(res.i128[0].cpu().numpy()))) == want
+
+
+@pytest.mark.parametrize("order", [3, 4, 5, 6])
+@pytest.mark.parametrize("offset,lo,hi", [(1024, -1024, 3071), (32768, -32768, 32767), (40000, -32768, 25535),
+                                          (1, -1, 5000)])
+def test_signed_exact_int16(order, offset, lo, hi):
+    """Signed-exact int16 (dpm_moments on layout-T volumes): the pass sums the raw
+    signed voxels (no per-voxel offset add) and the epilogue adds offset x the
+    box's moments; exact against the oracle on the offset uint16 volume, for
+    the extreme ends of the range, a batch, ragged shapes."""
+    rng = np.random.default_rng(order * 7 + offset % 97)
+    vols = rng.integers(lo, hi + 1, size=(3, 21, 13, 200), dtype=np.int64).astype(np.int16)
+    vols[0, :2] = lo                                   # both ends of the allowed range in one volume
+    vols[0, -2:] = hi
+    res = engine.moments(torch.from_numpy(vols).cuda(), order, offset=offset)
+    torch.cuda.synchronize()
+    assert res.status.cpu().numpy().max() == 0
+    idx = vm.moment_indices(order)
+    for b in range(3):
+        want = oracle.naive((vols[b].astype(np.int32) + offset).astype(np.uint16), order)
+        assert engine.i128_to_ints(res.i128[b].cpu().numpy()) == [want[k] for k in idx], b
+        assert np.isclose(res.f64[b].cpu().numpy()[0], float(want[(0, 0, 0)]))
