@@ -147,9 +147,17 @@ def dpm_moments_batch(volumes, order: int, check_consistency: bool = True, offse
     from . import engine
 
     engine.check_order(order)
-    vox = volumes if isinstance(volumes, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(volumes))
-    if not vox.is_cuda:
-        vox = vox.to("cuda")
+    if isinstance(volumes, torch.Tensor):
+        vox = volumes if volumes.is_cuda else volumes.to("cuda")
+    else:
+        arr = np.ascontiguousarray(volumes)
+        if arr.ndim != 4:
+            raise ValueError("batch must be [B, N, M, L]")
+        from .projection import _uploader
+        # large host batches: the threaded pinned-staging upload (volumes along the leading axis)
+        vox = _uploader().upload(arr) if arr.nbytes >= (32 << 20) else None
+        if vox is None:
+            vox = torch.from_numpy(arr).to("cuda")
     if vox.dim() != 4:
         raise ValueError("batch must be [B, N, M, L]")
     res = engine.moments(vox, order, offset=offset)

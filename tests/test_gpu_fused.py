@@ -105,3 +105,14 @@ def test_not_fused_outside_envelope():
         assert res.launches >= 3   # zeroing, projection, moments (+ epilogue)
         want = oracle.dpm(vol, order)
         assert engine.i128_to_ints(res.i128[0].cpu().numpy()) == [want[k] for k in vm.moment_indices(order)]
+
+
+def test_dropin_batch_from_host_numpy():
+    """dpm_moments_batch on a host numpy batch above the staging threshold: the
+    threaded pinned-staging upload (volumes along the leading axis), then the
+    fused pass; exact against the oracle."""
+    rng = np.random.default_rng(21)
+    vols = rng.integers(0, 256, size=(40, 128, 64, 128), dtype=np.uint8)   # 40 MB
+    got = vm.dpm_moments_batch(vols, 3)
+    for b in (0, 17, 39):
+        assert got[b].values == oracle.dpm(vols[b], 3), b
