@@ -150,21 +150,28 @@ __global__ void DPM_M2_BOUNDS moments2d_kernel(M2Params p) {
   for (int l = 0; l < NTP; ++l) acc[l] = 0;
   if (i < W) {
     const uint32_t* col = p.s.img[k] + b * W * H + j0 * W + i;
-    #pragma unroll M2_UNROLL
-    for (int rr = 0; rr < rows; ++rr) {
-      const uint32_t raw = __ldg(col + (int64_t)rr * W);
-      // signed pixels (sgn): sign-extended; the limb sums stay exact int64 (|v t| < 2^55, 256 rows)
-      const uint64_t v = p.sgn ? (uint64_t)(int64_t)(int32_t)raw : (uint64_t)raw;
-      const uint4* tr = reinterpret_cast<const uint4*>(&table[rr][0]);
-      #pragma unroll
-      for (int l4 = 0; l4 < NTP / 4; ++l4) {
-        const uint4 t = tr[l4];
-        acc[4 * l4 + 0] += v * t.x;
-        acc[4 * l4 + 1] += v * t.y;
-        acc[4 * l4 + 2] += v * t.z;
-        acc[4 * l4 + 3] += v * t.w;
+    // one 32 x 32 -> 64 multiply-add per limb (IMAD.WIDE): the pixel stays a
+    // 32-bit operand in both variants (a uint64 pixel times a limb costs three)
+    auto column = [&]<bool SGN>() {
+      #pragma unroll M2_UNROLL
+      for (int rr = 0; rr < rows; ++rr) {
+        const uint32_t raw = __ldg(col + (int64_t)rr * W);
+        const uint4* tr = reinterpret_cast<const uint4*>(&table[rr][0]);
+        #pragma unroll
+        for (int l4 = 0; l4 < NTP / 4; ++l4) {
+          const uint4 t = tr[l4];
+          const uint32_t tl[4] = {t.x, t.y, t.z, t.w};
+          #pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            // signed pixels (sgn): the limb sums stay exact int64 (|v t| < 2^55, 256 rows)
+            if constexpr (SGN) acc[4 * l4 + e] += (uint64_t)((int64_t)(int32_t)raw * (int64_t)(int32_t)tl[e]);
+            else acc[4 * l4 + e] += (uint64_t)raw * (uint64_t)tl[e];
+          }
+        }
       }
-    }
+    };
+    if (p.sgn) column.template operator()<true>();
+    else column.template operator()<false>();
   }
 
   __syncthreads();  // table dead from here on; its storage becomes red

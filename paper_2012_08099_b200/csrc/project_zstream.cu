@@ -84,6 +84,10 @@ __host__ __device__ constexpr int zs_spl(int K) { return (DPM_ZS_SPLIT && DPM_ZS
 #ifndef DPM_ZS_NW34
 #define DPM_ZS_NW34 12       // warps per CTA at orders 3-4
 #endif
+#ifndef DPM_ZS_EARLY_REL
+#define DPM_ZS_EARLY_REL 1   // release a stage once the step's last plane group is in registers, refill it at the step's end (x42: cfg5 -3 %)
+#endif
+
 #ifndef DPM_ZS_CS_FMA
 #define DPM_ZS_CS_FMA 0   // YZ-slot x sums with IMAD-by-1 (FMA pipe) instead of 3-input adds
 #endif
@@ -128,13 +132,13 @@ template <int AS> struct Ring {
   }
 };
 // CTA profile ring: live span 31 AS + 1 plus the warps' drift (< STAGES steps)
-// plus the flush lag (a block is flushed STAGES steps after it completes).
+// plus the flush lag (a block is flushed STAGES, with early release STAGES + 1, steps after it completes).
 // R is a power of two (a multiple of 32): for odd AS the lanes' blocks n + AS l
 // are 32 distinct banks as they are; for AS = 2 the two parity classes are
 // split into halves (slot (m & 1) R/2 + m/2), so no division by AS at all
 __host__ __device__ constexpr int zs_pow2_at_least(int v) { int r = 32; while (r < v) r *= 2; return r; }
 template <int AS, int STAGES> struct PRing {
-  static constexpr int R = zs_pow2_at_least(32 * AS + 2 * STAGES + 2);
+  static constexpr int R = zs_pow2_at_least(32 * AS + 2 * STAGES + 4);
   static constexpr int RP = R + 1;
   static constexpr int WORDS = 8 * RP;
   static __device__ __forceinline__ int idx(int b) {
@@ -216,13 +220,15 @@ template <> struct ZUnpack<int16_t> {   // sign-extend, add the offset (0 for ze
     }
   }
 };
-template <> struct ZUnpack<s16> {   // sign-extend only: PRMT (sign-replicate) + arithmetic shift
+template <> struct ZUnpack<s16> {   // sign-extend only: both halves by PRMT with sign replication
+  // (an arithmetic shift for the high half is fused into EVERY add that uses it
+  // as LEA.HI.SX32, a 2-input add: twice the adds of the 3-input pairs)
   template <typename V> __device__ __forceinline__ static void run(const V& d, uint32_t* v, int32_t, uint32_t) {
     const uint32_t* w = reinterpret_cast<const uint32_t*>(&d);
     #pragma unroll
     for (int i = 0; i < 4; ++i) {
       asm("prmt.b32 %0, %1, 0, 0x9910;" : "=r"(v[2 * i]) : "r"(w[i]));
-      v[2 * i + 1] = (uint32_t)((int32_t)w[i] >> 16);
+      asm("prmt.b32 %0, %1, 0, 0xBB32;" : "=r"(v[2 * i + 1]) : "r"(w[i]));
     }
   }
 };
@@ -606,7 +612,16 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
 #ifndef DPM_ZS_ZLAG
 #define DPM_ZS_ZLAG (K >= 6 ? 2 : 1)   // measured best per order (x26)
 #endif
-  constexpr int ZLAG = STAGES >= 4 ? DPM_ZS_ZLAG : 1;
+  // early release: the stage goes back to the producer once the step's last
+  // plane group is in registers, half a step before the step ends
+  constexpr bool EREL = DPM_ZS_EARLY_REL && zs_spl(K) == 1 && !ZLAST && !ZPW;
+  // ... and thread 0 refills it at the END of its own step (lag 0: it only waits
+  // for warps more than half a step behind it); without early release the
+  // refill is at the step's top, ZLAG steps behind
+  constexpr int ZLAG = EREL ? 0 : STAGES >= 4 ? DPM_ZS_ZLAG : 1;
+  // a refilled stage proves every warp RELEASED step g - STAGES; released early,
+  // that only proves step g - STAGES - 1 was emitted completely
+  constexpr int PLAG = STAGES + (EREL ? 1 : 0);
   constexpr int ZLAGS = ZLAG * SPL;   // the same lag in sub-stages
   static_assert(sizeof(ZProd) <= 96, "stage cursor budget (ZGeo::SMEM)");
   int k = 0, pw = 0, kl = 0, lagc = 0;
@@ -677,11 +692,11 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
       }
     };
     // step g's (last) sub-stage was refilled only after every warp released
-    // step g - STAGES: profile blocks <= rn - STAGES are complete; warp g mod NW
+    // step g - STAGES: profile blocks <= rn - PLAG are complete; warp g mod NW
     // flushes that one
     auto flush_profile_block = [&](const int rn) {
-      if (w == pw && rn >= STAGES && lane < 8) {
-        const int blk = rn - STAGES;
+      if (w == pw && rn >= PLAG && lane < 8) {
+        const int blk = rn - PLAG;
         const uint32_t a = pring_a + 4u * (uint32_t)(PR::idx(blk) + lane * PR::RP);
         const uint32_t v = ptx::lds_u32(a);
         ptx::sts_u32(a, 0u);
@@ -708,7 +723,7 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
       uint32_t yzmine = 0;
       uint32_t tile_a = 0;
       if constexpr (SPL == 1) {
-        produce();
+        if constexpr (!EREL) produce();
         if constexpr (DPM_ZS_SLEEP > 0) ptx::mbar_wait_addr_sleep(bar_a + 8u * (uint32_t)k, ph, DPM_ZS_SLEEP);
         else ptx::mbar_wait_addr(bar_a + 8u * (uint32_t)k, ph);
         flush_profile_block(rn);
@@ -750,6 +765,11 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
           const uint32_t r = __reduce_add_sync(0xffffffffu, sm);
           if constexpr (DPM_ZS_XY_SMEM) ptx::sts_u32(ptx::smem_addr(xyv + GP * h + gg), r);   // uniform value, one word
           else yzmine = lane == GP * h + gg ? r : yzmine;
+        }
+        if constexpr (EREL) {
+          // every plane of the stage has been read AND used (the reductions above
+          // consumed each lane's loaded words), so the stage can be refilled now
+          if (h == 8 / GP - 1) release();
         }
         // YZ slot: x-sums over z
         #pragma unroll
@@ -804,8 +824,9 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
         ptx::sts_u32(a, 0u);
         ptx::red_global_add_if(fptr + 8 * rn, v, v != 0 && (uint32_t)(rn - frlo) < frange);
       }
-      if constexpr (SPL == 1) release();
+      if constexpr (SPL == 1 && !EREL) release();
       else __syncwarp();
+      if constexpr (EREL) produce();
       if (++pw == NW) pw = 0;
     };
     auto end_emit = [&]<int R>(const int rn_end) {
@@ -877,7 +898,7 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
     // CTA profile ring: every warp has emitted all of the segment; flush what is left
     zs_sync<NW>();
     {
-      const int first = rn_end >= STAGES ? rn_end - STAGES : 0;   // blocks the step loop did not flush
+      const int first = rn_end >= PLAG ? rn_end - PLAG : 0;   // blocks the step loop did not flush
       const int nblk = rn_end + 32 * ASP - first;
       for (int c = tid; c < 8 * nblk; c += 32 * NW) {
         const int blk = first + c / 8, kk = c % 8;
