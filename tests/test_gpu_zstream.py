@@ -144,3 +144,30 @@ def test_signed_exact_int16(order, offset, lo, hi):
         want = oracle.naive((vols[b].astype(np.int32) + offset).astype(np.uint16), order)
         assert engine.i128_to_ints(res.i128[b].cpu().numpy()) == [want[k] for k in idx], b
         assert np.isclose(res.f64[b].cpu().numpy()[0], float(want[(0, 0, 0)]))
+
+
+def test_x_tile_major_column_order():
+    """Large image sets order the columns x-tile outermost (project_zstream.cu,
+    zdecode).  DPM_ZS_XT_MAJOR_MB=0 selects that order for a small volume in a
+    fresh process: orders 4 and 6, three x-tiles, partial tiles, vs the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import numpy as np, torch, oracle\n"
+        "import paper_2012_08099_b200 as vm\n"
+        "from paper_2012_08099_b200 import engine\n"
+        "rng = np.random.default_rng(77)\n"
+        "for shape, order in (((40, 50, 712), 6), ((24, 37, 520), 4)):\n"
+        "    vol = rng.integers(0, 65536, size=shape).astype(np.uint16)\n"
+        "    res = engine.moments(torch.from_numpy(vol).cuda(), order)\n"
+        "    torch.cuda.synchronize()\n"
+        "    assert int(res.status[0]) == 0\n"
+        "    want = oracle.dpm(vol, order)\n"
+        "    got = engine.i128_to_ints(res.i128[0].cpu().numpy())\n"
+        "    assert got == [want[k] for k in vm.moment_indices(order)], (shape, order)\n"
+        "print('xt-major ok')\n")
+    env = dict(os.environ, DPM_ZS_XT_MAJOR_MB="0", PYTHONPATH=root)
+    proc = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=root, timeout=600)
+    assert proc.returncode == 0 and "xt-major ok" in proc.stdout, proc.stdout + proc.stderr
