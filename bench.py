@@ -462,6 +462,8 @@ def main():
         "config": workload_config(cfg, world, cache_note(cfg)),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
+                     # the same bytes over the WHOLE step (zeroing, moments and epilogue launches included)
+                     "frac_step": round(my_bytes / (ms_max / args.steps * 1e-3) / 1e9 / peak, 4),
                      "kernel": "zstream_kernel (the layout-T projection pass alone; its buffers are re-zeroed by the moments stage)" if cfg == 5 else "whole pipeline (one graph replay)",
                      "traffic": tr},
         "cpu_baseline": cpu,

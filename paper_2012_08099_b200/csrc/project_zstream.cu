@@ -117,6 +117,7 @@ struct ZParams {
   int32_t zsplit;                // round-robin mode: segments per column
   int32_t run_mode;              // 1: equal contiguous runs of the (column, step) space
   int32_t xt_major;              // column order: 1 = x-tile outermost, 0 = x-tile innermost
+  int32_t small;                 // ncol * ns < 2^31: segment arithmetic in 32 bits
   uint32_t one;                  // == 1 at run time (IMAD-by-1 folds on the FMA pipe)
   uint32_t* img[DPM_MAX_IMAGES];
   int64_t W[DPM_MAX_IMAGES];     // stored widths (layout T)
@@ -441,7 +442,9 @@ struct ZSeg {
   __device__ __forceinline__ void set_run(const ZParams& p) {
     done = pos >= end;
     if (done) return;
-    col = pos / p.ns;
+    // 32-bit division when the step space allows it (a 64-bit division is a
+    // ~100-instruction dependent chain on the column-end critical path)
+    col = p.small ? (int64_t)((uint32_t)pos / (uint32_t)p.ns) : pos / p.ns;
     n0 = (int32_t)(pos - col * p.ns);
     n1 = (int32_t)imin64(p.ns, n0 + (end - pos));
   }
@@ -469,6 +472,17 @@ struct ZProd {
 // same time, so their image rows are still in L2 -- worth it once the image
 // set is larger than L2 (cfg5: DRAM 18.75 -> 18.10 GB per launch, pass -1.2 %)
 __device__ __forceinline__ void zdecode(const ZParams& p, int64_t col, int32_t& xt, int32_t& yg, int32_t& b) {
+  if (p.small) {   // everything fits 32 bits
+    const uint32_t c = (uint32_t)col;
+    const uint32_t inner = p.xt_major ? (uint32_t)p.n_yg : (uint32_t)p.n_xt;
+    const uint32_t outer = p.xt_major ? (uint32_t)p.n_xt : (uint32_t)p.n_yg;
+    const uint32_t r = c / inner, i0 = c - r * inner;
+    const uint32_t bb = r / outer, i1 = r - bb * outer;
+    xt = (int32_t)(p.xt_major ? i1 : i0);
+    yg = (int32_t)(p.xt_major ? i0 : i1);
+    b = (int32_t)bb;
+    return;
+  }
   if (p.xt_major) {
     yg = (int32_t)(col % p.n_yg);
     const int64_t r = col / p.n_yg;
@@ -620,7 +634,11 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
   // this lane's share of the per-step ring flush: form fj, cell fk of the completed block
   const int fj = lane >> 3, fk = lane & 7;
   const int fas = fj < 2 ? 1 : 2;                     // |s| of form fj
-  const uint32_t fring_a = wring_a + (fj == 0 ? R0 : fj == 1 ? R1 : fj == 2 ? R2 : R3) + 4u * (uint32_t)(fk * (32 * fas + 1));
+#ifndef DPM_ZS_FBASE_OPAQUE
+#define DPM_ZS_FBASE_OPAQUE 0   // keep the lane's flush base address in a register (ptxas rematerializes it from the lane id every step: ~24 instructions)
+#endif
+  uint32_t fring_a = wring_a + (fj == 0 ? R0 : fj == 1 ? R1 : fj == 2 ? R2 : R3) + 4u * (uint32_t)(fk * (32 * fas + 1));
+  if constexpr (DPM_ZS_FBASE_OPAQUE) asm volatile("" : "+r"(fring_a));
   const int lpp = lane, lpm = 31 - lane;             // lane l' of forms with s > 0 / s < 0
 
   // step counter (all warps): step g in stage k / phase ph; step g - ZLAG in stage kl /
@@ -835,7 +853,14 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
       // the ring block this step completed: lanes 8j..8j+7 flush form j's 8 cells
       if (fj < NOB) {
         const int m = rn & (32 * fas - 1);
-        const uint32_t a = fring_a + 4u * (uint32_t)((m & (fas - 1)) * 32 + (m >> (fas - 1)));
+        uint32_t a;
+        if constexpr (DPM_ZS_FBASE_OPAQUE) {
+          const uint32_t s1 = ((uint32_t)rn & 31u) << 2;
+          const uint32_t s2 = (((uint32_t)rn & 1u) << 7) | ((((uint32_t)rn >> 1) & 31u) << 2);
+          a = fring_a + (lane >= 16 ? s2 : s1);
+        } else {
+          a = fring_a + 4u * (uint32_t)((m & (fas - 1)) * 32 + (m >> (fas - 1)));
+        }
         const uint32_t v = ptx::lds_u32(a);
         ptx::sts_u32(a, 0u);
         ptx::red_global_add_if(fptr + 8 * rn, v, v != 0 && (uint32_t)(rn - frlo) < frange);
@@ -897,6 +922,7 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
       const uint32_t roff = j == 0 ? R0 : j == 1 ? R1 : j == 2 ? R2 : R3;
       const int32_t base = base_of(s), Wj = (int32_t)p.W[DPM_IMG_DIAG + j];
       uint32_t* const rowj = p.img[DPM_IMG_DIAG + j] + rowid * Wj;
+      #pragma unroll
       for (int c = lane; c < 8 * 32 * as; c += 32) {
         const int blk = rn_end + c / 8, kk = c % 8;
         const int idx = as == 1 ? Ring<1>::idx(blk) : Ring<2>::idx(blk);
@@ -991,6 +1017,7 @@ static int launch_zs(const dpm_volume_desc* d, const void* vox, const ImageSet& 
   p.n_yg = (int32_t)((d->M + NW - 1) / NW);
   p.ns = (int32_t)((d->N + 7) / 8);
   p.ncol = d->B * p.n_yg * p.n_xt;
+  p.small = p.ncol * p.ns < 0x7fffffffLL;
   p.one = 1;
   for (int k = 0; k < DPM_MAX_IMAGES; ++k) { p.img[k] = s.img[k]; p.W[k] = s.W[k]; }
   p.prof = prof;

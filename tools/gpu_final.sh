@@ -12,7 +12,7 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > ${O}_bench_r
 for g in 2 4 8; do timeout 900 python bench.py --simulate-ranks $g --steps 5 >> ${O}_simulate_ranks_cfg5.jsonl 2>> ${O}_bench_err.log; done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file ${O}_cfg5_launches.csv \
   python bench.py --config 5 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file ${O}_cfg4_launches.csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"fused|zero_kernel|moments2d|derive" -c 60 --csv --log-file ${O}_cfg4_launches.csv \
   python bench.py --config 4 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:zstream -s 1 -c 1 -o ${O}_cfg5_zstream -f \
   python bench.py --config 5 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1

@@ -40,7 +40,8 @@ def main():
             name = r["Kernel Name"].split("(")[0].replace("void ", "")
             per[name].append(float(r["Metric Value"]) / 1e6)
     step = {k: v for k, v in per.items() if "synth" not in k}
-    n_steps = max(len(v) for v in step.values())
+    # steps = launches of the dominant kernel (helper kernels may launch several times per step)
+    n_steps = len(max(step.values(), key=lambda v: sum(v)))
     step_ms = sum(sum(v) for v in step.values()) / n_steps
 
     raw = list(csv.reader(io.StringIO(ncu(rep, "--page", "raw", "--csv"))))

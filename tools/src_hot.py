@@ -16,6 +16,7 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 root = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2012_08099_b200", "csrc")
 cur, ncol, S, E = None, None, None, None
 agg = collections.defaultdict(lambda: [0.0, 0.0])
+text = {}
 for L in out.splitlines():
     if L.startswith('"File Path"'):
         cur = L.split(",")[1].strip('"').split("/")[-1]
@@ -37,9 +38,10 @@ for L in out.splitlines():
         continue
     agg[(cur, ln)][0] += s
     agg[(cur, ln)][1] += e
+    text.setdefault((cur, ln), parts[1] if len(parts) > 1 else "")   # the source text embedded in the report
 ts = sum(v[0] for v in agg.values())
 te = sum(v[1] for v in agg.values())
 print(f"samples {ts:.0f}, warp instructions {te:.0f}")
 for (f, ln), (s, e) in sorted(agg.items(), key=lambda kv: -kv[1][by])[:n]:
-    src = linecache.getline(os.path.join(root, f), ln).strip()[:84]
+    src = (text.get((f, ln)) or linecache.getline(os.path.join(root, f), ln)).strip()[:84]
     print(f"{f}:{ln:4d} samp {s / ts:6.2%} inst {e / te:6.2%}  {src}")
