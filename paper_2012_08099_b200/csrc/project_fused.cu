@@ -118,18 +118,21 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) fused_batch_kernel(const __g
   const int64_t r0 = p.total * blockIdx.x / gridDim.x, r1 = p.total * (blockIdx.x + 1) / gridDim.x;
   if (r0 >= r1) return;
   for (int i = tid; i < 3 * fb::ROWW + fb::PROFW; i += T) rows[i] = 0;
-  auto issue = [&](int64_t r, int k) {
-    const int64_t b = r / p.M;
-    const int32_t y = (int32_t)(r - b * p.M);
+  // refill cursor (thread 0): the next row to fetch, advanced row by row -- no
+  // division in the row loop (a 64-bit division is a call, and a call site in
+  // the loop costs every thread registers)
+  int32_t ib = (int32_t)(r0 / p.M);
+  int32_t iy = (int32_t)(r0 - (int64_t)ib * p.M);
+  auto issue = [&](int k) {
     ptx::mbar_arrive_expect_tx(&full[k], G::STAGE);
-    ptx::tma_load_4d_hint(stages + (size_t)k * G::STAGE, &tmap, &full[k], 0, y, 0, (int32_t)b,
-                          ptx::policy_evict_first());
+    ptx::tma_load_4d_hint(stages + (size_t)k * G::STAGE, &tmap, &full[k], 0, iy, 0, ib, ptx::policy_evict_first());
+    if (++iy == (int32_t)p.M) { iy = 0; ++ib; }
   };
   if (tid == 0) {
     ptx::prefetch_tmap(&tmap);
     for (int i = 0; i < S; ++i) ptx::mbar_init(&full[i], 1);
     ptx::fence_barrier_init();
-    for (int h = 0; h < S && r0 + h < r1; ++h) issue(r0 + h, h);
+    for (int h = 0; h < S && r0 + h < r1; ++h) issue(h);
   }
   __syncthreads();
 
@@ -298,7 +301,7 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) fused_batch_kernel(const __g
     }
   };
 
-  int64_t b = r0 / p.M;
+  int64_t b = (int32_t)(r0 / p.M);
   int32_t y = (int32_t)(r0 - b * p.M);
   int32_t seg_rows = 0, pq_rows = 0;
   int k = 0, buf = 0;
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) fused_batch_kernel(const __g
     const uint32_t yzp = __shfl_sync(0xffffffffu, yz2, lane >> 1);
     const uint32_t yzv = (lane & 1) ? (yzp >> 16) : (yzp & 0xFFFFu);
     __syncthreads();
-    if (tid == 0 && r + S < r1) issue(r + S, k);
+    if (tid == 0 && r + S < r1) issue(k);
     if (++k == S) { k = 0; ph ^= 1u; }
 
     // ---- fold the completed rows of this row-step into the y-power accumulators ----

@@ -45,11 +45,9 @@
 //              row y per step (red.global, partial over x-tiles).
 //   YZ slot  = the lane's VX x-sums over all planes of the segment (registers),
 //              flushed at the end of the segment.
-// Work split: the (column, step) space is cut into segments (a column = one
-// (volume, y-group, x-tile); a segment = a run of its z-steps), assigned round
-// robin so that the CTAs running at any moment work on neighbouring y-groups
-// (their image rows stay L2-resident), or as equal contiguous runs when all
-// images fit in L2 anyway (perfect balance).
+// Work split: the (column, step) space (a column = one (volume, y-group,
+// x-tile), a step = 8 of its planes) is cut into equal contiguous runs, one
+// per persistent CTA; a segment = the part of a run inside one column.
 // Exactness: uint32 ray sums (the C ABI rejects shapes whose longest ray could
 // reach 2^32), integer atomics: order independent, bit-identical.
 #include <cudaTypedefs.h>
@@ -70,9 +68,6 @@ __host__ __device__ constexpr int zs_ctas(int K) { return K >= 5 ? DPM_ZS_CTAS6 
 #endif
 #ifndef DPM_ZS_SLEEP
 #define DPM_ZS_SLEEP 0   // suspend-time hint (ns) of the stage waits; 0 = plain try_wait polling
-#endif
-#ifndef DPM_ZS_RUN_MB
-#define DPM_ZS_RUN_MB (1 << 20)   // image sets up to this size (MB): equal contiguous runs; larger: round robin (x34: runs always win)
 #endif
 #ifndef DPM_ZS_HALF_MINK
 #define DPM_ZS_HALF_MINK 5   // lowest order that uses the group-wise windows
@@ -114,10 +109,7 @@ struct ZParams {
   int32_t offset;
   int32_t n_xt, n_yg, ns;        // x-tiles, y-groups, z-steps per column
   int64_t ncol;                  // B * n_yg * n_xt
-  int32_t zsplit;                // round-robin mode: segments per column
-  int32_t run_mode;              // 1: equal contiguous runs of the (column, step) space
   int32_t xt_major;              // column order: 1 = x-tile outermost, 0 = x-tile innermost
-  int32_t small;                 // ncol * ns < 2^31: segment arithmetic in 32 bits
   uint32_t one;                  // == 1 at run time (IMAD-by-1 folds on the FMA pipe)
   uint32_t* img[DPM_MAX_IMAGES];
   int64_t W[DPM_MAX_IMAGES];     // stored widths (layout T)
@@ -417,44 +409,32 @@ __device__ __forceinline__ void zemit_group_tail(uint32_t (&win)[NWIN], uint32_t
 }
 
 // Segment iterator shared by the producer and the consumers: the CTA's
-// sequence of (column, n0, n1) step ranges.
+// sequence of (column, n0, n1) step ranges -- its equal contiguous run of the
+// flattened (column, step) space, cut at the column ends.  All of it fits 32
+// bits (a step is >= 16 KB of voxels: 2^31 steps would be 32 TB), and must:
+// a 64-bit division is a ~100-instruction call, and call sites inside the
+// step loop cost the whole loop registers (x47: cfg5 pass -4 %)
 struct ZSeg {
-  int64_t col;
+  uint32_t col;
   int32_t n0, n1;
-  // round robin: unit index; run mode: position in the flattened step space
-  int64_t u, pos, end;
+  uint32_t pos, end;     // position in the flattened step space, end of the run
   bool done;
   __device__ __forceinline__ void first(const ZParams& p) {
-    if (p.run_mode) {
-      const int64_t W = p.ncol * p.ns;
-      pos = W * blockIdx.x / gridDim.x;
-      end = W * (blockIdx.x + 1) / gridDim.x;
-      set_run(p);
-    } else {
-      u = blockIdx.x;
-      set_rr(p);
-    }
+    const uint64_t W = (uint64_t)p.ncol * (uint64_t)p.ns;
+    pos = (uint32_t)(W * blockIdx.x / gridDim.x);
+    end = (uint32_t)(W * (blockIdx.x + 1) / gridDim.x);
+    set_run(p);
   }
   __device__ __forceinline__ void next(const ZParams& p) {
-    if (p.run_mode) { pos += n1 - n0; set_run(p); }
-    else { u += gridDim.x; set_rr(p); }
+    pos += (uint32_t)(n1 - n0);
+    set_run(p);
   }
   __device__ __forceinline__ void set_run(const ZParams& p) {
     done = pos >= end;
     if (done) return;
-    // 32-bit division when the step space allows it (a 64-bit division is a
-    // ~100-instruction dependent chain on the column-end critical path)
-    col = p.small ? (int64_t)((uint32_t)pos / (uint32_t)p.ns) : pos / p.ns;
-    n0 = (int32_t)(pos - col * p.ns);
-    n1 = (int32_t)imin64(p.ns, n0 + (end - pos));
-  }
-  __device__ __forceinline__ void set_rr(const ZParams& p) {
-    done = u >= p.ncol * p.zsplit;
-    if (done) return;
-    col = u / p.zsplit;
-    const int32_t zc = (int32_t)(u - col * p.zsplit);
-    n0 = (int32_t)((int64_t)zc * p.ns / p.zsplit);
-    n1 = (int32_t)((int64_t)(zc + 1) * p.ns / p.zsplit);
+    col = pos / (uint32_t)p.ns;
+    n0 = (int32_t)(pos - col * (uint32_t)p.ns);
+    n1 = (int32_t)umin((uint32_t)p.ns, (uint32_t)n0 + (end - pos));
   }
 };
 
@@ -471,29 +451,14 @@ struct ZProd {
 // x-tile outermost: the x-tiles of a y-group run on different CTAs at about the
 // same time, so their image rows are still in L2 -- worth it once the image
 // set is larger than L2 (cfg5: DRAM 18.75 -> 18.10 GB per launch, pass -1.2 %)
-__device__ __forceinline__ void zdecode(const ZParams& p, int64_t col, int32_t& xt, int32_t& yg, int32_t& b) {
-  if (p.small) {   // everything fits 32 bits
-    const uint32_t c = (uint32_t)col;
-    const uint32_t inner = p.xt_major ? (uint32_t)p.n_yg : (uint32_t)p.n_xt;
-    const uint32_t outer = p.xt_major ? (uint32_t)p.n_xt : (uint32_t)p.n_yg;
-    const uint32_t r = c / inner, i0 = c - r * inner;
-    const uint32_t bb = r / outer, i1 = r - bb * outer;
-    xt = (int32_t)(p.xt_major ? i1 : i0);
-    yg = (int32_t)(p.xt_major ? i0 : i1);
-    b = (int32_t)bb;
-    return;
-  }
-  if (p.xt_major) {
-    yg = (int32_t)(col % p.n_yg);
-    const int64_t r = col / p.n_yg;
-    xt = (int32_t)(r % p.n_xt);
-    b = (int32_t)(r / p.n_xt);
-  } else {
-    xt = (int32_t)(col % p.n_xt);
-    const int64_t r = col / p.n_xt;
-    yg = (int32_t)(r % p.n_yg);
-    b = (int32_t)(r / p.n_yg);
-  }
+__device__ __forceinline__ void zdecode(const ZParams& p, uint32_t col, int32_t& xt, int32_t& yg, int32_t& b) {
+  const uint32_t inner = p.xt_major ? (uint32_t)p.n_yg : (uint32_t)p.n_xt;
+  const uint32_t outer = p.xt_major ? (uint32_t)p.n_xt : (uint32_t)p.n_yg;
+  const uint32_t r = col / inner, i0 = col - r * inner;
+  const uint32_t bb = r / outer, i1 = r - bb * outer;
+  xt = (int32_t)(p.xt_major ? i1 : i0);
+  yg = (int32_t)(p.xt_major ? i0 : i1);
+  b = (int32_t)bb;
 }
 
 // Who refills a stage (DPM_ZS_PWARP):
@@ -634,11 +599,7 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
   // this lane's share of the per-step ring flush: form fj, cell fk of the completed block
   const int fj = lane >> 3, fk = lane & 7;
   const int fas = fj < 2 ? 1 : 2;                     // |s| of form fj
-#ifndef DPM_ZS_FBASE_OPAQUE
-#define DPM_ZS_FBASE_OPAQUE 0   // keep the lane's flush base address in a register (ptxas rematerializes it from the lane id every step: ~24 instructions)
-#endif
-  uint32_t fring_a = wring_a + (fj == 0 ? R0 : fj == 1 ? R1 : fj == 2 ? R2 : R3) + 4u * (uint32_t)(fk * (32 * fas + 1));
-  if constexpr (DPM_ZS_FBASE_OPAQUE) asm volatile("" : "+r"(fring_a));
+  const uint32_t fring_a = wring_a + (fj == 0 ? R0 : fj == 1 ? R1 : fj == 2 ? R2 : R3) + 4u * (uint32_t)(fk * (32 * fas + 1));
   const int lpp = lane, lpm = 31 - lane;             // lane l' of forms with s > 0 / s < 0
 
   // step counter (all warps): step g in stage k / phase ph; step g - ZLAG in stage kl /
@@ -853,14 +814,7 @@ __global__ void __launch_bounds__(32 * (NW + ZPW), zs_ctas(K)) zstream_kernel(co
       // the ring block this step completed: lanes 8j..8j+7 flush form j's 8 cells
       if (fj < NOB) {
         const int m = rn & (32 * fas - 1);
-        uint32_t a;
-        if constexpr (DPM_ZS_FBASE_OPAQUE) {
-          const uint32_t s1 = ((uint32_t)rn & 31u) << 2;
-          const uint32_t s2 = (((uint32_t)rn & 1u) << 7) | ((((uint32_t)rn >> 1) & 31u) << 2);
-          a = fring_a + (lane >= 16 ? s2 : s1);
-        } else {
-          a = fring_a + 4u * (uint32_t)((m & (fas - 1)) * 32 + (m >> (fas - 1)));
-        }
+        const uint32_t a = fring_a + 4u * (uint32_t)((m & (fas - 1)) * 32 + (m >> (fas - 1)));
         const uint32_t v = ptx::lds_u32(a);
         ptx::sts_u32(a, 0u);
         ptx::red_global_add_if(fptr + 8 * rn, v, v != 0 && (uint32_t)(rn - frlo) < frange);
@@ -1017,38 +971,22 @@ static int launch_zs(const dpm_volume_desc* d, const void* vox, const ImageSet& 
   p.n_yg = (int32_t)((d->M + NW - 1) / NW);
   p.ns = (int32_t)((d->N + 7) / 8);
   p.ncol = d->B * p.n_yg * p.n_xt;
-  p.small = p.ncol * p.ns < 0x7fffffffLL;
   p.one = 1;
   for (int k = 0; k < DPM_MAX_IMAGES; ++k) { p.img[k] = s.img[k]; p.W[k] = s.W[k]; }
   p.prof = prof;
   p.WQ = WQ;
-  // schedule: images that fit in L2 -> equal contiguous runs; else round robin
-  // over z-split segments (chosen for balance, segments >= 8 steps)
+  // schedule: equal contiguous runs of the (column, step) space, one per CTA
+  // (32-bit positions: see ZSeg); column order by the size of the image set
+  if (p.ncol * p.ns >= 0x7fffffffLL) return -1;   // not reachable with < 32 TB of voxels: the classic pass takes it
   int64_t img_bytes = 0;
   for (int k = 0; k < s.n_img; ++k) img_bytes += s.W[k] * s.H[k] * 4 * d->B;
   const int64_t G_ = (int64_t)sms * zs_ctas(K);
-  if (img_bytes <= ((int64_t)DPM_ZS_RUN_MB << 20) || p.ncol * p.ns < 4 * G_) {
-    p.run_mode = 1;
-    p.zsplit = 1;
-    // (the threshold can be overridden at run time, e.g. 0 to test the order on small volumes)
-    static const int64_t xt_mb = [] { const char* e = getenv("DPM_ZS_XT_MAJOR_MB"); return e ? (int64_t)atoll(e) : (int64_t)DPM_ZS_XT_MAJOR_MB; }();
-    p.xt_major = img_bytes > (xt_mb << 20) && p.n_xt > 1;
-  } else {
-    double best = -1.0;
-    int bz = 1;
-    for (int zs = 1; zs <= imax64(1, p.ns / 8); ++zs) {
-      const int64_t U = p.ncol * zs;
-      const int64_t rounds = (U + G_ - 1) / G_;
-      const double steps = (double)p.ns / zs;
-      const double score = (double)U / (double)(rounds * G_) * steps / (steps + 2.0);
-      if (score > best + 1e-9) { best = score; bz = zs; }
-    }
-    p.zsplit = bz;
-  }
+  // (the threshold can be overridden at run time, e.g. 0 to test the order on small volumes)
+  static const int64_t xt_mb = [] { const char* e = getenv("DPM_ZS_XT_MAJOR_MB"); return e ? (int64_t)atoll(e) : (int64_t)DPM_ZS_XT_MAJOR_MB; }();
+  p.xt_major = img_bytes > (xt_mb << 20) && p.n_xt > 1;
   static std::atomic<uint64_t> attr_mask{0};
   if (ensure_smem(zstream_kernel<T, K, NW, VX, S, C::FMAMASK>, G::SMEM, attr_mask)) return DPM_ECUDA;
-  const int64_t units = p.run_mode ? p.ncol * p.ns : p.ncol * p.zsplit;
-  const int grid = (int)imin64(G_, units);
+  const int grid = (int)imin64(G_, p.ncol * p.ns);
   if (launch_pdl(zstream_kernel<T, K, NW, VX, S, C::FMAMASK>, dim3(grid), dim3(32 * (NW + ZPW)), G::SMEM, st, map, p) !=
       cudaSuccess)
     return DPM_ECUDA;
