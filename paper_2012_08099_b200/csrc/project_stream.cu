@@ -237,13 +237,20 @@ template <int VX> __device__ __forceinline__ uint32_t sumv(const uint32_t* v) {
 struct Cursor {
   int32_t y0, yb, c, yoff, left;
   bool done;
-  __device__ void band_setup(const StreamParams& p) {
+  // floor(seq * i / g) without a 64-bit division (a call: call sites reachable
+  // from the row-step loop cost the loop its register allocation); the host
+  // guarantees seq < 2^31 (a row-step is >= 4 KB of voxels)
+  static __device__ __forceinline__ uint32_t share(uint32_t seq, uint32_t i, uint32_t g) {
+    const uint32_t q = seq / g, r = seq - q * g;
+    return q * i + (r * i) / g;
+  }
+  __device__ __forceinline__ void band_setup(const StreamParams& p) {
     while (y0 < p.M) {
       yb = (int32_t)imin64(p.band, p.M - y0);
-      const int64_t seq = p.ncol * yb;
-      const int64_t s = (seq * blockIdx.x) / gridDim.x;
-      const int64_t e = (seq * (blockIdx.x + 1)) / gridDim.x;
-      if (s < e) { c = (int32_t)(s / yb); yoff = (int32_t)(s - (int64_t)c * yb); left = (int32_t)(e - s); done = false; return; }
+      const uint32_t seq = (uint32_t)p.ncol * (uint32_t)yb;
+      const uint32_t s = share(seq, blockIdx.x, gridDim.x);
+      const uint32_t e = share(seq, blockIdx.x + 1, gridDim.x);
+      if (s < e) { c = (int32_t)(s / (uint32_t)yb); yoff = (int32_t)(s - (uint32_t)c * (uint32_t)yb); left = (int32_t)(e - s); done = false; return; }
       y0 += (int32_t)p.band;
     }
     done = true;
@@ -826,6 +833,7 @@ static int launch_one(const dpm_volume_desc* d, const void* vox, int grid, cudaS
   p.ntx = (d->L + G::SX - 1) / G::SX;
   p.ntz = (d->N + G::SZ - 1) / G::SZ;
   p.ncol = p.ntx * p.ntz * d->B;
+  if (p.ncol * d->M >= 0x7fffffffLL) return -1;   // 32-bit row-step positions (Cursor); not reachable in 180 GB
   p.single = (DPM_SINGLE_TILE && PROF && p.ntx == 1 && p.ntz == 1) ? 1u : 0u;
   static std::atomic<uint64_t> attr_mask{0};
   if (ensure_smem(project_stream_kernel<T, NI, NW, VX, S, PROF, ZP, CTAS>, bytes, attr_mask)) return DPM_ECUDA;
