@@ -109,7 +109,7 @@ struct ZParams {
   int32_t offset;
   int32_t n_xt, n_yg, ns;        // x-tiles, y-groups, z-steps per column
   int64_t ncol;                  // B * n_yg * n_xt
-  int32_t xt_major;              // column order: 1 = x-tile outermost, 0 = x-tile innermost
+  int32_t yb;                    // column order: y-groups per block (zdecode)
   uint32_t one;                  // == 1 at run time (IMAD-by-1 folds on the FMA pipe)
   uint32_t* img[DPM_MAX_IMAGES];
   int64_t W[DPM_MAX_IMAGES];     // stored widths (layout T)
@@ -446,18 +446,24 @@ struct ZProd {
   int32_t xt, yg, b;     // decoded column of seg
   int32_t hh;            // next half of step n (DPM_ZS_SPLIT)
 };
-// Column order.  x-tile innermost: a CTA's run walks the x-tiles of one y-group
-// one after the other (they add into the same image rows a column later).
-// x-tile outermost: the x-tiles of a y-group run on different CTAs at about the
-// same time, so their image rows are still in L2 -- worth it once the image
-// set is larger than L2 (cfg5: DRAM 18.75 -> 18.10 GB per launch, pass -1.2 %)
+// Column order: volume, then blocks of p.yb y-groups, then the x-tile, then the
+// y-group inside the block.  yb = 1 is x-tile innermost: a CTA's run walks the
+// x-tiles of one y-group one after the other (they add into the same image
+// rows a column later; fine while the image set fits in L2).  For larger image
+// sets the x-tiles of a y-group should run on DIFFERENT CTAs at the SAME time,
+// so that a row's partial sums meet in L2: two columns run simultaneously when
+// their indices differ by a multiple of the run length R = ncol / grid, so the
+// host picks yb = round(m R) for the small m with the least rounding error
+// (cfg5: R = 9.24, yb = 37 = 4.003 R); yb = n_yg is plain x-tile-outermost order.
 __device__ __forceinline__ void zdecode(const ZParams& p, uint32_t col, int32_t& xt, int32_t& yg, int32_t& b) {
-  const uint32_t inner = p.xt_major ? (uint32_t)p.n_yg : (uint32_t)p.n_xt;
-  const uint32_t outer = p.xt_major ? (uint32_t)p.n_xt : (uint32_t)p.n_yg;
-  const uint32_t r = col / inner, i0 = col - r * inner;
-  const uint32_t bb = r / outer, i1 = r - bb * outer;
-  xt = (int32_t)(p.xt_major ? i1 : i0);
-  yg = (int32_t)(p.xt_major ? i0 : i1);
+  const uint32_t per_vol = (uint32_t)p.n_yg * (uint32_t)p.n_xt;
+  const uint32_t bb = col / per_vol, c = col - bb * per_vol;
+  const uint32_t per_blk = (uint32_t)p.yb * (uint32_t)p.n_xt;
+  const uint32_t blk = c / per_blk, w = c - blk * per_blk;
+  const uint32_t ybt = umin((uint32_t)p.yb, (uint32_t)p.n_yg - blk * (uint32_t)p.yb);   // the last block may be short
+  const uint32_t x = w / ybt;
+  xt = (int32_t)x;
+  yg = (int32_t)(blk * (uint32_t)p.yb + (w - x * ybt));
   b = (int32_t)bb;
 }
 
@@ -981,12 +987,25 @@ static int launch_zs(const dpm_volume_desc* d, const void* vox, const ImageSet& 
   int64_t img_bytes = 0;
   for (int k = 0; k < s.n_img; ++k) img_bytes += s.W[k] * s.H[k] * 4 * d->B;
   const int64_t G_ = (int64_t)sms * zs_ctas(K);
+  const int grid = (int)imin64(G_, p.ncol * p.ns);
   // (the threshold can be overridden at run time, e.g. 0 to test the order on small volumes)
   static const int64_t xt_mb = [] { const char* e = getenv("DPM_ZS_XT_MAJOR_MB"); return e ? (int64_t)atoll(e) : (int64_t)DPM_ZS_XT_MAJOR_MB; }();
-  p.xt_major = img_bytes > (xt_mb << 20) && p.n_xt > 1;
+  static const int yb_forced = [] { const char* e = getenv("DPM_ZS_YB"); return e ? atoi(e) : 0; }();
+  p.yb = 1;
+  if (img_bytes > (xt_mb << 20) && p.n_xt > 1) {
+    const double R = (double)p.ncol / grid;
+    double best = 1e9;
+    p.yb = p.n_yg;
+    for (int m = 1; m <= 8; ++m) {
+      const int yb = (int)(m * R + 0.5);
+      if (yb < 1 || yb > p.n_yg) continue;
+      const double err = fabs(yb - m * R);
+      if (err < best - 1e-9) { best = err; p.yb = yb; }
+    }
+    if (yb_forced > 0) p.yb = (int)imin64(yb_forced, p.n_yg);
+  }
   static std::atomic<uint64_t> attr_mask{0};
   if (ensure_smem(zstream_kernel<T, K, NW, VX, S, C::FMAMASK>, G::SMEM, attr_mask)) return DPM_ECUDA;
-  const int grid = (int)imin64(G_, p.ncol * p.ns);
   if (launch_pdl(zstream_kernel<T, K, NW, VX, S, C::FMAMASK>, dim3(grid), dim3(32 * (NW + ZPW)), G::SMEM, st, map, p) !=
       cudaSuccess)
     return DPM_ECUDA;

@@ -146,10 +146,13 @@ def test_signed_exact_int16(order, offset, lo, hi):
         assert np.isclose(res.f64[b].cpu().numpy()[0], float(want[(0, 0, 0)]))
 
 
-def test_x_tile_major_column_order():
-    """Large image sets order the columns x-tile outermost (project_zstream.cu,
-    zdecode).  DPM_ZS_XT_MAJOR_MB=0 selects that order for a small volume in a
-    fresh process: orders 4 and 6, three x-tiles, partial tiles, vs the oracle."""
+@pytest.mark.parametrize("yb", [2, 4, 100])
+def test_blocked_column_order(yb):
+    """Large image sets order the columns in blocks of y-groups with the x-tile
+    outermost inside a block (project_zstream.cu, zdecode).  DPM_ZS_XT_MAJOR_MB=0
+    selects that order for small volumes in a fresh process and DPM_ZS_YB sets
+    the block size (2, 4: short last blocks; 100: one block = plain x-tile
+    outermost): orders 4 and 6, three x-tiles, partial tiles, vs the oracle."""
     import os
     import subprocess
     import sys
@@ -167,7 +170,7 @@ def test_x_tile_major_column_order():
         "    want = oracle.dpm(vol, order)\n"
         "    got = engine.i128_to_ints(res.i128[0].cpu().numpy())\n"
         "    assert got == [want[k] for k in vm.moment_indices(order)], (shape, order)\n"
-        "print('xt-major ok')\n")
-    env = dict(os.environ, DPM_ZS_XT_MAJOR_MB="0", PYTHONPATH=root)
+        "print('blocked order ok')\n")
+    env = dict(os.environ, DPM_ZS_XT_MAJOR_MB="0", DPM_ZS_YB=str(yb), PYTHONPATH=root)
     proc = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=root, timeout=600)
-    assert proc.returncode == 0 and "xt-major ok" in proc.stdout, proc.stdout + proc.stderr
+    assert proc.returncode == 0 and "blocked order ok" in proc.stdout, proc.stdout + proc.stderr
