@@ -30,8 +30,10 @@
 //   step     = 8 planes: ONE 4-D TMA box (x SX, y NW, z 8, b 1) per step into a
 //              STAGES-deep ring with full/empty mbarriers.  No CTA barrier per
 //              step: each warp releases a stage by arriving on its empty
-//              barrier; the producer (warp 0) refills a stage once all warps
-//              released it, so warps drift freely within the ring.
+//              barrier as soon as the step's last planes are in registers
+//              (mid-step); thread 0 refills the stage at the end of its own
+//              step once all warps released it, so warps drift freely within
+//              the ring.
 //   lane     = VX consecutive x of the warp's row, 8 planes per step.
 //   forms    = register windows of 8 + |s|(VX-1) cells, slid by 8 cells per
 //              step; the 8 completed cells go to a warp-private ring of image
@@ -39,8 +41,8 @@
 //              blocks are consecutive ring slots), and the warp flushes the one
 //              ring block that completes per step to global memory (8 cells per
 //              form, red.global).  The profile window goes to a CTA-shared
-//              ring (it is summed over the warps' y), flushed by warp 0 once
-//              every warp is past the block.
+//              ring (it is summed over the warps' y), flushed block by block
+//              by the warps in turn once every warp is past the block.
 //   XY slot  = per-plane lane sums, one warp redux per plane, 8 plane sums of
 //              row y per step (red.global, partial over x-tiles).
 //   YZ slot  = the lane's VX x-sums over all planes of the segment (registers),
@@ -438,8 +440,7 @@ struct ZSeg {
   }
 };
 
-// producer state in shared memory: the producer duty rotates over the warps
-// (step g's refill is issued by warp g mod NW), so no warp is slower than the rest
+// producer state (thread 0's refill cursor), kept in shared memory to spare registers
 struct ZProd {
   ZSeg seg;
   int32_t n, k;          // next step to issue (within seg), its stage (sub-stage with DPM_ZS_SPLIT)
