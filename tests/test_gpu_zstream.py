@@ -152,7 +152,8 @@ def test_blocked_column_order(yb):
     outermost inside a block (project_zstream.cu, zdecode).  DPM_ZS_XT_MAJOR_MB=0
     selects that order for small volumes in a fresh process and DPM_ZS_YB sets
     the block size (2, 4: short last blocks; 100: one block = plain x-tile
-    outermost): orders 4 and 6, three x-tiles, partial tiles, vs the oracle."""
+    outermost): orders 4 and 6, three x-tiles, partial tiles, and a batch of
+    three volumes at order 5, vs the oracle."""
     import os
     import subprocess
     import sys
@@ -170,6 +171,13 @@ def test_blocked_column_order(yb):
         "    want = oracle.dpm(vol, order)\n"
         "    got = engine.i128_to_ints(res.i128[0].cpu().numpy())\n"
         "    assert got == [want[k] for k in vm.moment_indices(order)], (shape, order)\n"
+        "vols = rng.integers(0, 65536, size=(3, 16, 40, 520)).astype(np.uint16)\n"
+        "res = engine.moments(torch.from_numpy(vols).cuda(), 5)\n"
+        "torch.cuda.synchronize()\n"
+        "for b in range(3):\n"
+        "    want = oracle.dpm(vols[b], 5)\n"
+        "    assert int(res.status[b]) == 0\n"
+        "    assert engine.i128_to_ints(res.i128[b].cpu().numpy()) == [want[k] for k in vm.moment_indices(5)], b\n"
         "print('blocked order ok')\n")
     env = dict(os.environ, DPM_ZS_XT_MAJOR_MB="0", DPM_ZS_YB=str(yb), PYTHONPATH=root)
     proc = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=root, timeout=600)
